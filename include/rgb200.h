@@ -1,0 +1,135 @@
+/*
+ * rgb200.h — C ABI of librgb200.so, the sm_100a hot path of block GCRO-DR
+ * (block recycled GMRES, arXiv 1604.01713) behind the recgmres Python API.
+ *
+ * Conventions (every entry point):
+ *   - Plain pointers and sizes; no torch / numpy types.  All pointers named
+ *     d_* are DEVICE pointers owned by the caller; the library never
+ *     allocates device memory.  Scratch memory is caller-provided and sized
+ *     with rg_*_workspace_bytes().  The workspace counter word must be zero
+ *     when first handed to the library (the kernels leave it zero again).
+ *   - Dense blocks are column-major (Fortran order, like the reference's
+ *     as_block, sparse_core.py:51-58) with a leading dimension ld >= n.
+ *   - `stream` is a cudaStream_t passed as void*; every call is
+ *     stream-ordered and asynchronous (no host synchronisation inside).
+ *   - Return value: RG_OK (0) on success, RG_EBADARG (1) for bad shapes /
+ *     arguments (the Python layer raises ShapeError/ValueError, as the
+ *     reference does), RG_ECUDA (2) for a CUDA launch error.  The message of
+ *     the last failure on the calling thread is available from
+ *     rg_last_error().
+ *   - Floating point is IEEE float64 throughout.
+ */
+#ifndef RGB200_H
+#define RGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_OK 0
+#define RG_EBADARG 1
+#define RG_ECUDA 2
+
+/* Library identification: returns a static string "rgb200 <version> sm_100a". */
+const char* rg_version(void);
+
+/* Message of the last failing call on this thread ("" when none). */
+const char* rg_last_error(void);
+
+/* Number of SMs of the current device (for grid sizing / diagnostics). */
+int rg_device_sm_count(void);
+
+/*
+ * Y = A * X for a CSR matrix A and an n_cols x p block X.
+ *
+ * Replaces recgmres.sparse_core.spmm -> _spmm_kernel
+ * (/root/reference/pkg/src/recgmres/sparse_core.py:132-149 and :25-40) and
+ * spmv (:152-157).  Every output entry Y[i,c] is accumulated from 0.0 over
+ * the row's stored nonzeros in ascending storage order with separately
+ * rounded multiply and add (no FMA) — the reference kernel's exact
+ * arithmetic, so results are bitwise identical to it.
+ *
+ * Rows [row_begin, row_end) are computed (row-range launches let the
+ * distributed layer overlap interior rows with the halo exchange).  Column
+ * indices j < n_local read X[j + c*ldx]; j >= n_local read the ghost block
+ * Xg[(j - n_local) + c*ldg] (pass n_local = n_cols, d_xg = NULL on one GPU).
+ * row_ptr / col_idx are int32 (nnz < 2^31).
+ */
+int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_end,
+                    const int32_t* d_row_ptr, const int32_t* d_col_idx,
+                    const double* d_vals,
+                    const double* d_x, int64_t ldx, int64_t n_local,
+                    const double* d_xg, int64_t ldg,
+                    int32_t p, double* d_y, int64_t ldy, void* stream);
+
+/*
+ * Fused tall-skinny "update, triangular solve, Gram" pass over an n x p
+ * block Z (one read of every operand, one write of Z):
+ *
+ *   z   = (d_zin ? Zin : 0)                       (n x p)
+ *   z  += alpha1 * (X1 @ S1)                      X1: n x a1, S1: a1 x p
+ *   z  += alpha2 * (X2 @ S2)                      X2: n x a2, S2: a2 x p
+ *   z   = z @ inv(R1)   if d_r1                   R1: p x p upper triangular
+ *   z   = z @ inv(R2)   if d_r2
+ *   Zout = z            if d_zout (may alias Zin)
+ *   gram_mode 1:  Gout = Gb^T @ z                 Gb: n x gc, Gout: gc x p
+ *   gram_mode 2:  Gout = z^T @ z                  (gc must equal p)
+ *   gram_mode 3:  Gout[c] = sum_i z[i,c]^2        (column sums of squares)
+ *
+ * S1/S2/R1/R2 and Gout are DEVICE arrays, column-major with ld = rows.
+ * Gram sums are reduced in a fixed order (deterministic run to run).
+ *
+ * Replaces the numpy/OpenBLAS products of the hot path:
+ *   arnoldi.step CGS2 branch   arnoldi.py:172-180   (C^T Ahat, Ahat -= C S,
+ *                                                    W^T Ahat, Ahat -= W c)
+ *   reduced_qr Gram / apply    dense_kernels.py:41  (CholQR2 passes)
+ *   C-scrubs                   solver.py:155, :266-267, :281, :297
+ *   _apply_update              solver.py:175-179
+ *   recycle products           recycling.py:119-120, :165-169, :186-188
+ *   column norms               solver.py:214, :274, :299, :321
+ */
+int rg_tall_f64(int64_t n, int32_t p,
+                const double* d_zin, int64_t ldzin,
+                double* d_zout, int64_t ldzout,
+                const double* d_x1, int64_t ldx1, int32_t a1,
+                const double* d_s1, double alpha1,
+                const double* d_x2, int64_t ldx2, int32_t a2,
+                const double* d_s2, double alpha2,
+                const double* d_r1, const double* d_r2,
+                int32_t gram_mode, const double* d_gb, int64_t ldgb, int32_t gc,
+                double* d_gout,
+                void* d_work, int64_t work_bytes, void* stream);
+
+/* Workspace bytes rg_tall_f64 needs for these shapes. */
+int64_t rg_tall_workspace_bytes(int64_t n, int32_t p, int32_t a1, int32_t a2,
+                                int32_t gram_mode, int32_t gc);
+
+/*
+ * Cholesky G = R^T R of a p x p SPD Gram (device, column-major, ld = p),
+ * p <= 64.  Writes R (upper, ld = p; strictly-lower part zeroed) and
+ * d_status[0]: 0 ok; 1 not positive definite / non-finite; 2 ill
+ * conditioned (min_j R_jj^2 < cond_tol * max_j G_jj).  Used by the CholQR2
+ * path of reduced_qr (dense_kernels.py:31-48); status != 0 sends the block
+ * to the Householder TSQR path instead.
+ */
+int rg_chol_f64(int32_t p, const double* d_g, double* d_r, int32_t* d_status,
+                double cond_tol, void* stream);
+
+/*
+ * Householder TSQR of an n x p block (p <= 32), in place:  X = Q R with Q
+ * overwriting X and R (p x p, upper, ld = p) written to d_r.  Signs follow
+ * the reference convention R_jj >= 0 (dense_kernels.py:42-45).  This is the
+ * robust path of reduced_qr (np.linalg.qr, dense_kernels.py:41), used when
+ * CholQR2 declines (near rank-deficient blocks, breakdown handling).
+ */
+int rg_tsqr_f64(int64_t n, int32_t p, double* d_x, int64_t ldx, double* d_r,
+                void* d_work, int64_t work_bytes, void* stream);
+int64_t rg_tsqr_workspace_bytes(int64_t n, int32_t p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RGB200_H */

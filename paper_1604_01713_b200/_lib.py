@@ -1,0 +1,90 @@
+"""ctypes binding of librgb200.so (include/rgb200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is present, every device entry point raises instead of silently
+computing on the host.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import pathlib
+import threading
+
+_PKG = pathlib.Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "librgb200.so"
+
+RG_OK, RG_EBADARG, RG_ECUDA = 0, 1, 2
+
+c_i32, c_i64, c_dbl, c_ptr = ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+
+# name -> (restype, argtypes); mirrors include/rgb200.h
+PROTOTYPES = {
+    "rg_version": (ctypes.c_char_p, []),
+    "rg_last_error": (ctypes.c_char_p, []),
+    "rg_device_sm_count": (ctypes.c_int, []),
+    "rg_spmm_csr_f64": (ctypes.c_int, [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
+                                       c_ptr, c_i64, c_i32, c_ptr, c_i64, c_ptr]),
+    "rg_tall_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_i64,
+                                   c_ptr, c_i64, c_i32, c_ptr, c_dbl,
+                                   c_ptr, c_i64, c_i32, c_ptr, c_dbl,
+                                   c_ptr, c_ptr, c_i32, c_ptr, c_i64, c_i32, c_ptr,
+                                   c_ptr, c_i64, c_ptr]),
+    "rg_tall_workspace_bytes": (c_i64, [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32]),
+    "rg_chol_f64": (ctypes.c_int, [c_i32, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr]),
+    "rg_tsqr_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
+    "rg_tsqr_workspace_bytes": (c_i64, [c_i64, c_i32]),
+    "rg_spmm_csr_c128": (ctypes.c_int, [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
+                                        c_ptr, c_i64, c_i32, c_ptr, c_i64, c_ptr]),
+    "rg_tall_c128": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_i64,
+                                    c_ptr, c_i64, c_i32, c_ptr, c_dbl,
+                                    c_ptr, c_i64, c_i32, c_ptr, c_dbl,
+                                    c_ptr, c_ptr, c_i32, c_ptr, c_i64, c_i32, c_ptr,
+                                    c_ptr, c_i64, c_ptr]),
+    "rg_tall_c128_workspace_bytes": (c_i64, [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32]),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class KernelError(RuntimeError):
+    """A CUDA launch inside librgb200 failed."""
+
+
+def load(required_symbols=None):
+    """Load librgb200.so (building it first if it is absent and nvcc exists)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            from . import build as _build
+
+            _build.build()
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, (res, args) in PROTOTYPES.items():
+            fn = getattr(lib, name, None)
+            if fn is None:
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def exported_symbols():
+    lib = load()
+    return sorted(n for n in PROTOTYPES if getattr(lib, n, None) is not None)
+
+
+def check(rc: int, what: str):
+    """Map an rg_* status to the reference's exception classes."""
+    if rc == RG_OK:
+        return
+    msg = (_lib.rg_last_error() or b"").decode(errors="replace") if _lib is not None else ""
+    if rc == RG_EBADARG:
+        from .sparse_core import ShapeError
+
+        raise ShapeError(f"{what}: {msg}")
+    raise KernelError(f"{what}: {msg}")

@@ -1,0 +1,307 @@
+"""Block Arnoldi with the recycle-space projection, device resident.
+
+Drop-in for ``recgmres.arnoldi`` (/root/reference/pkg/src/recgmres/
+arnoldi.py): ``ArnoldiFactorization``, ``start``, ``step``,
+``ZeroStartBlock`` with the reference's signatures and semantics.
+
+State placement: the basis W = [V_1 ... V_{m_max+1}] is one
+column-major n x (m_max+1)L block in HBM; the small H, F and z_bar stay on
+the host (the progressive least-squares problem and the harmonic Ritz
+problem read them there).  One step is
+
+    Ahat = A V_m                       rg_spmm_csr_f64 (or the user closure)
+    CGS2 vs C then W, twice            ortho.project_chain -> 5 rg_tall passes
+    Ahat = V_{m+1} R                   CholQR2 (Gram fused into the last CGS2
+                                       pass) or Householder TSQR fallback
+    one D2H of all small coefficients  (the only host sync of the step)
+
+and the host accumulates F, H exactly as arnoldi.py:177,180,183 do.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import device as _dev
+from .dense_kernels import QrScratch, _flags, cholqr2_finish, cholqr2_launch, tsqr_into
+from .ortho import project_chain
+from .sparse_core import ShapeError
+
+
+class ZeroStartBlock(ValueError):
+    """The starting block is numerically zero (already converged)."""
+
+
+class ArnoldiFactorization:
+    """State of the block Arnoldi iteration (arnoldi.py:22-95).
+
+    w        : basis blocks V_1..V_{m+1}, a CUDA n x (m+1)L column-major view
+    h_bar    : block upper-Hessenberg (m+1)L x mL (host)
+    f        : C-projection coefficients k x mL (host)
+    z_bar    : L x L R-factor of the starting block (host)
+    m        : completed block steps
+    """
+
+    def __init__(self, n: int, L: int, m_max: int, k: int, rank_tol: float, seed: int, device=None):
+        self.n = n
+        self.L = L
+        self.m_max = m_max
+        self.k = k
+        self.rank_tol = rank_tol
+        self.m = 0
+        dev = _dev.require_cuda(device)
+        self.device = dev
+        self._W = _dev.empty_block(n, (m_max + 1) * L, dev)
+        self._H = np.zeros(((m_max + 1) * L, m_max * L))
+        self._F = np.zeros((k, m_max * L))
+        self.z_bar = np.zeros((L, L))
+        self.breakdown_events: list[str] = []
+        self._rng = np.random.default_rng(seed)
+        self._ahat = _dev.empty_block(n, L, dev)
+        # packed small coefficients of one step: S1 | c1 | S2 | c2 (column-major blocks)
+        wmax = (m_max + 1) * L
+        self._coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=torch.float64, device=dev)
+        self._coef_host = torch.zeros_like(self._coef, device="cpu").pin_memory()
+        self._qr = QrScratch(L, dev)
+        self._qr_host = torch.zeros(5 * L * L, dtype=torch.float64).pin_memory()
+        self._st_host = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self.launches = 0  # rg_* kernel launches issued by start/step (diagnostics)
+
+    # ---- views (arnoldi.py:47-76)
+    @property
+    def w(self) -> torch.Tensor:
+        return self._W[:, : (self.m + 1) * self.L]
+
+    @property
+    def h_bar(self) -> np.ndarray:
+        return self._H[: (self.m + 1) * self.L, : self.m * self.L]
+
+    @property
+    def f(self) -> np.ndarray:
+        return self._F[:, : self.m * self.L]
+
+    def h_square(self) -> np.ndarray:
+        return self._H[: self.m * self.L, : self.m * self.L]
+
+    def h_last_block(self) -> np.ndarray:
+        mL = self.m * self.L
+        return self._H[mL: mL + self.L, mL - self.L: mL]
+
+    def v_block(self, i: int) -> torch.Tensor:
+        return self._W[:, i * self.L: (i + 1) * self.L]
+
+    def new_hbar_columns(self) -> np.ndarray:
+        mL = self.m * self.L
+        return self._H[: mL + self.L, mL - self.L: mL]
+
+    def w_numpy(self) -> np.ndarray:
+        """Host copy of the active basis (D2H; for tests / small problems)."""
+        return _dev.to_numpy_block(self.w)
+
+    def _coef_views(self, m: int):
+        k, L, w = self.k, self.L, (m + 1) * self.L
+        sizes = [k * L, w * L, k * L, w * L]
+        rows = [k, w, k, w]
+        out, off = [], 0
+        for s, r in zip(sizes, rows):
+            out.append(self._coef[off: off + s].view(L, r).t() if r else self._coef[off:off].view(L, 0).t())
+            off += s
+        return out
+
+    def _unit_vector_into(self, col: torch.Tensor, v: torch.Tensor, nrm: float):
+        """col = v / nrm (division on the device, as the reference's v / nrm)."""
+        r = torch.full((1, 1), nrm, dtype=torch.float64, device=self.device)
+        _dev.tall(v, col, r1=r)
+
+    def _random_direction(self, bases, tries=3):
+        """Seeded replacement direction: host PCG64 normals (same stream as the
+        reference), CGS twice against ``bases`` on the device.  Returns
+        (vector, norm) or (None, 0)."""
+        scratch = [torch.zeros(b.shape[1], dtype=torch.float64, device=self.device).view(-1, 1) for b in bases]
+        for _ in range(tries):
+            v = _dev.to_device_block(self._rng.standard_normal(self.n).reshape(-1, 1))
+            for _pass in range(2):
+                project_chain(v, v, bases, [s[: b.shape[1]] for s, b in zip(scratch, bases)])
+            ss = torch.zeros(1, dtype=torch.float64, device=self.device)
+            _dev.tall(v, None, gram=("sumsq", ss))
+            nrm = float(np.sqrt(ss.item()))
+            if nrm > 1e-8:
+                return v, nrm
+        return None, 0.0
+
+
+def _as_block_on(x, dev):
+    if isinstance(x, torch.Tensor):
+        if x.dim() == 1:
+            x = x.reshape(-1, 1)
+        if x.dim() != 2:
+            raise ShapeError(f"expected a vector or 2-D block, got ndim={x.dim()}")
+        return _dev.to_device_block(x, dev)
+    a = np.asarray(x, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    if a.ndim != 2:
+        raise ShapeError(f"expected a vector or 2-D block, got ndim={a.ndim}")
+    return _dev.to_device_block(a, dev)
+
+
+def _apply_operator(opA, Z: torch.Tensor, out: torch.Tensor):
+    """out = opA(Z); operators exposing ``apply_into`` write in place."""
+    into = getattr(opA, "apply_into", None)
+    if into is None:
+        owner = getattr(opA, "__self__", None)
+        into = getattr(owner, "apply_into", None) if owner is not None and getattr(opA, "__name__", "") == "apply" else None
+    if into is not None:
+        into(Z, out)
+        return
+    Y = opA(Z)
+    if not isinstance(Y, torch.Tensor):
+        Y = _dev.to_device_block(np.asarray(Y, dtype=np.float64), Z.device)
+    if Y.dim() == 1:
+        Y = Y.reshape(-1, 1)
+    if tuple(Y.shape) != tuple(out.shape):
+        raise ValueError("operator closure returned a block of wrong shape")
+    out.copy_(Y)
+
+
+def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: int = 0,
+          device=None) -> ArnoldiFactorization:
+    """Initialise from the starting block R0 (arnoldi.py:98-136): V_1, z_bar
+    from its thin QR; rank-deficient columns replaced by seeded random
+    directions (C- and V_1-orthogonalised twice) and logged."""
+    dev = _dev.require_cuda(device if device is not None else
+                            (R0.device if isinstance(R0, torch.Tensor) and R0.is_cuda else None))
+    R0d = _as_block_on(R0, dev)
+    n, L = R0d.shape
+    ss = torch.zeros(L, dtype=torch.float64, device=dev)
+    _dev.tall(R0d, None, gram=("sumsq", ss))
+    norm0 = float(np.sqrt(ss.sum().item()))
+    if norm0 == 0.0 or not np.isfinite(norm0):
+        raise ZeroStartBlock("starting block is numerically zero")
+    k = recycle.k if recycle is not None else 0
+    fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev)
+    V1 = fact.v_block(0)
+    qr = _block_qr(fact, R0d, V1)
+    fact.z_bar = qr[0]
+    flagged = qr[1]
+    C = recycle.c_device() if recycle is not None else None
+    for j in np.flatnonzero(flagged):
+        # the reference projects against C, then V1 without column j (arnoldi.py:115-123)
+        others = [c for c in range(L) if c != j]
+        bases = ([C] if C is not None else []) + ([_dev.to_device_block(V1[:, others])] if others else [])
+        v, nrm = fact._random_direction(bases)
+        if v is not None:
+            fact._unit_vector_into(V1[:, j: j + 1], v, nrm)
+        else:
+            V1[:, j].zero_()
+        fact.breakdown_events.append(f"start: replaced rank-deficient column {j}"
+                                     + ("" if v is not None else " (space exhausted, column zeroed)"))
+    return fact
+
+
+def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False):
+    """Thin QR X -> Q (Q must not alias X).  Returns (R, flagged)."""
+    L = X.shape[1]
+    scr = fact._qr
+    if L <= _dev.MAX_P:
+        cholqr2_launch(X, Q, scr, g1_ready=g1_ready)
+        fact._qr_host.copy_(scr.buf, non_blocking=True)
+        fact._st_host.copy_(scr.status, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        ok, R, norm_x = cholqr2_finish(fact._qr_host.numpy(), fact._st_host.numpy(), L)
+        if ok:
+            return R, _flags(R, norm_x, fact.rank_tol)
+    else:
+        _dev.tall(X, None, gram=("sumsq", scr.buf[:L]))
+        norm_x = float(np.sqrt(scr.buf[:L].sum().item()))
+    tsqr_into(X, Q, scr)
+    R = np.triu(scr.RT.cpu().numpy())
+    return R, _flags(R, norm_x, fact.rank_tol)
+
+
+def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> ArnoldiFactorization:
+    """Advance by one block step (arnoldi.py:139-193)."""
+    if fact.m >= fact.m_max:
+        raise ValueError(f"factorization at capacity m_max={fact.m_max}")
+    if ortho not in ("mgs", "cgs2"):
+        raise ValueError(f"unknown orthogonalization '{ortho}'")
+    m, L = fact.m, fact.L
+    cols = slice(m * L, (m + 1) * L)
+    Vm = fact.v_block(m)
+    Ahat = fact._ahat
+    _apply_operator(opA, Vm, Ahat)
+    C = recycle.c_device() if recycle is not None else None
+    active = fact._W[:, : (m + 1) * L]
+    scr = fact._qr
+    Vnew = fact.v_block(m + 1)
+
+    if ortho == "cgs2":
+        S1, c1, S2, c2 = fact._coef_views(m)
+        if C is not None:
+            bases, coefs = [C, active, C, active], [S1, c1, S2, c2]
+        else:
+            bases, coefs = [active, active], [c1, c2]
+        project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.MAX_P else None)
+        ncoef = (2 * fact.k + 2 * (m + 1) * L) * L
+        fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
+        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.MAX_P)
+        hc = fact._coef_host.numpy()
+        k, w = fact.k, (m + 1) * L
+        off = 0
+        blocks = []
+        for rows in (k, w, k, w):
+            blocks.append(hc[off: off + rows * L].reshape(L, rows).T)
+            off += rows * L
+        hS1, hc1, hS2, hc2 = blocks
+        if C is not None:
+            fact._F[:, cols] += hS1
+            fact._F[:, cols] += hS2
+        fact._H[: (m + 1) * L, cols] += hc1
+        fact._H[: (m + 1) * L, cols] += hc2
+    else:
+        _mgs_project(fact, Ahat, C, m, cols)
+        R, flagged = _block_qr(fact, Ahat, Vnew)
+
+    fact._H[(m + 1) * L: (m + 2) * L, cols] = R
+    for j in np.flatnonzero(flagged):
+        bases = ([C] if C is not None else []) + [active, Vnew]
+        v, nrm = fact._random_direction(bases)
+        if v is not None:
+            fact._unit_vector_into(Vnew[:, j: j + 1], v, nrm)
+        else:
+            Vnew[:, j].zero_()
+        fact.breakdown_events.append(f"step {m + 1}: replaced rank-deficient basis column {j}"
+                                     + ("" if v is not None else " (space exhausted, column zeroed)"))
+    fact.m = m + 1
+    return fact
+
+
+def _mgs_project(fact, Ahat, C, m, cols):
+    """Block modified Gram-Schmidt (arnoldi.py:159-170): one vector of C at a
+    time, then one basis block at a time; each pass fuses the previous
+    update with the next Gram."""
+    L = fact.L
+    bases = []
+    if C is not None:
+        bases += [C[:, i: i + 1] for i in range(C.shape[1])]
+    bases += [fact.v_block(i) for i in range(m + 1)]
+    coef = torch.zeros(sum(b.shape[1] for b in bases) * L, dtype=torch.float64, device=fact.device)
+    views, off = [], 0
+    for b in bases:
+        a = b.shape[1]
+        views.append(coef[off: off + a * L].view(L, a).t())
+        off += a * L
+    project_chain(Ahat, Ahat, bases, views)
+    hc = coef.cpu().numpy()
+    off = 0
+    kk = C.shape[1] if C is not None else 0
+    for i, b in enumerate(bases):
+        a = b.shape[1]
+        blk = hc[off: off + a * L].reshape(L, a).T
+        off += a * L
+        if i < kk:
+            fact._F[i, cols] += blk[0]
+        else:
+            bi = i - kk
+            fact._H[bi * L: (bi + 1) * L, cols] += blk

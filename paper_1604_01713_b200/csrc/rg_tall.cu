@@ -1,0 +1,428 @@
+// Fused tall-skinny block kernels (K2 Gram, K3 update, K4 CGS2 passes, the
+// CholQR2 passes of K5, K6 norms, K7 triangular solve, K8 scaling).
+//
+// One launch streams an n x p block Z once, tile by tile (R = 256 rows):
+//
+//   phase 1 (one thread per row):
+//       z  = Zin[i,:] (or 0)
+//       z += alpha_t * (X_t[i,:] @ S_t)      t = 1, 2; S_t staged in smem and
+//                                             read as warp broadcasts
+//       z  = z @ inv(R1) [@ inv(R2)]         row-wise forward substitution
+//       Zout[i,:] = z;  tile[:, r] = z       column-major smem tile
+//   phase 2 (Gram on the FP64 tensor cores, DMMA m8n8k4):
+//       Gout += Gb[tile rows, :]^T @ tile     (mode 1; A fragments are read
+//                                             straight from HBM: 8 columns x
+//                                             4 consecutive rows = 8 full
+//                                             32-byte sectors per warp load)
+//       Gout += tile^T @ tile                 (mode 2, CholQR Gram)
+//       Gout += column sums of z^2            (mode 3, norms; CUDA cores)
+//   epilogue: warp partials summed in warp order in smem -> CTA partial in
+//       the workspace -> the last CTA to finish sums the partials in CTA
+//       order (deterministic) into Gout and re-arms the ticket counter.
+//
+// This is the B200 restatement of the numpy/OpenBLAS calls the reference
+// makes per block Arnoldi step (arnoldi.py:172-180: S = C^T Ahat;
+// Ahat -= C S; coef = W^T Ahat; Ahat -= W coef; twice).  The host schedules
+// each launch as "the pending update + the next Gram", so every basis is
+// streamed once per dependency level rather than once per BLAS call.  The
+// Gram accumulators live in DMMA fragments (2 doubles per lane per 8x8 tile)
+// instead of per-lane outer-product blocks, which is what lets one CTA cover
+// an 80-column basis without spilling.  tcgen05 has no f64 kind, so DMMA is
+// the FP64 tensor path on sm_100a.
+#include "rg_common.cuh"
+
+namespace rg {
+
+constexpr int kTallThreads = 256;  // = tile rows R
+constexpr int kTallWarps = kTallThreads / 32;
+constexpr int kTileStride = kTallThreads + 4;  // padded: conflict-free DMMA fragment loads
+
+struct TallParams {
+  int64_t n;
+  int p;
+  const double* zin;
+  int64_t ldzin;
+  double* zout;
+  int64_t ldzout;
+  const double* x1;
+  int64_t ldx1;
+  int a1;
+  const double* s1;
+  double alpha1;
+  const double* x2;
+  int64_t ldx2;
+  int a2;
+  const double* s2;
+  double alpha2;
+  const double* r1;
+  const double* r2;
+  int gmode;  // 0 none, 1 basis, 2 self, 3 column sums of squares
+  const double* gb;
+  int64_t ldgb;
+  int gc;
+  int mtiles;  // ceil(gc / 8)
+  double* gout;
+  double* part;            // [grid][gc*p] (modes 1/2) or [grid][p] (mode 3)
+  unsigned int* counter;   // ticket
+  int64_t ntiles;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int PM>
+__device__ __forceinline__ void apply_term(double (&z)[PM], const double* __restrict__ X,
+                                           int64_t ldx, int a, const double* sS, double alpha,
+                                           int64_t i) {
+  double m[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) m[c] = 0.0;
+  int aa = 0;
+  // batches of 8 independent column loads keep enough bytes in flight
+  for (; aa + 8 <= a; aa += 8) {
+    double xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = __ldg(X + i + (int64_t)(aa + u) * ldx);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double* srow = sS + (aa + u) * PM;
+#pragma unroll
+      for (int c = 0; c < PM; ++c) m[c] = fma(xv[u], srow[c], m[c]);
+    }
+  }
+  for (; aa < a; ++aa) {
+    const double xv = __ldg(X + i + (int64_t)aa * ldx);
+    const double* srow = sS + aa * PM;
+#pragma unroll
+    for (int c = 0; c < PM; ++c) m[c] = fma(xv, srow[c], m[c]);
+  }
+  // numpy order: M = X @ S first, then Z -/+ M
+#pragma unroll
+  for (int c = 0; c < PM; ++c) z[c] = z[c] + alpha * m[c];
+}
+
+template <int PM>
+__device__ __forceinline__ void trsm_row(double (&z)[PM], const double* sR, int p) {
+  // y R = z with R upper triangular (row-major [i*PM + j] in smem)
+#pragma unroll
+  for (int j = 0; j < PM; ++j) {
+    if (j < p) {
+      double y = z[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) y = fma(-z[k], sR[k * PM + j], y);
+      z[j] = y / sR[j * PM + j];
+    }
+  }
+}
+
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kTallThreads, 1) tall_kernel(TallParams P) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;  // tile columns (zero padded to the MMA N)
+  constexpr int NT = PM8 / 8;
+  extern __shared__ __align__(16) double smem[];
+  const int p = P.p;
+  double* sS1 = smem;
+  double* sS2 = sS1 + P.a1 * PM;
+  double* sR1 = sS2 + P.a2 * PM;
+  double* sR2 = sR1 + (P.r1 ? PM * PM : 0);
+  double* sZ = sR2 + (P.r2 ? PM * PM : 0);  // [PM8][kTileStride]
+  double* sRed = sZ + ((P.gmode == 1 || P.gmode == 2) ? PM8 * kTileStride : 0);
+
+  for (int e = threadIdx.x; e < P.a1 * PM; e += kTallThreads) {
+    const int aa = e / PM, c = e % PM;
+    sS1[e] = c < p ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
+  }
+  for (int e = threadIdx.x; e < P.a2 * PM; e += kTallThreads) {
+    const int aa = e / PM, c = e % PM;
+    sS2[e] = c < p ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
+  }
+  if (P.r1)
+    for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
+      const int ii = e / PM, jj = e % PM;
+      sR1[e] = (ii < p && jj < p) ? P.r1[ii + (int64_t)jj * p] : (ii == jj ? 1.0 : 0.0);
+    }
+  if (P.r2)
+    for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
+      const int ii = e / PM, jj = e % PM;
+      sR2[e] = (ii < p && jj < p) ? P.r2[ii + (int64_t)jj * p] : (ii == jj ? 1.0 : 0.0);
+    }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const bool gram_tile = (P.gmode == 1 || P.gmode == 2);
+  const int mtiles = P.mtiles;
+
+  double acc[MTMAX][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MTMAX; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    const int64_t tile0 = tile * kTallThreads;
+    // ---------------- phase 1: row-wise update / solve / store
+    {
+      const int64_t i = tile0 + threadIdx.x;
+      double z[PM];
+#pragma unroll
+      for (int c = 0; c < PM; ++c) z[c] = 0.0;
+      if (i < P.n) {
+        if (P.zin) {
+#pragma unroll
+          for (int c = 0; c < PM; ++c)
+            if (c < p) z[c] = __ldg(P.zin + i + (int64_t)c * P.ldzin);
+        }
+        if (P.a1) apply_term<PM>(z, P.x1, P.ldx1, P.a1, sS1, P.alpha1, i);
+        if (P.a2) apply_term<PM>(z, P.x2, P.ldx2, P.a2, sS2, P.alpha2, i);
+        if (P.r1) trsm_row<PM>(z, sR1, p);
+        if (P.r2) trsm_row<PM>(z, sR2, p);
+        if (P.zout) {
+#pragma unroll
+          for (int c = 0; c < PM; ++c)
+            if (c < p) P.zout[i + (int64_t)c * P.ldzout] = z[c];
+        }
+        if (P.gmode == 3) {
+#pragma unroll
+          for (int c = 0; c < PM; ++c) sq[c] = fma(z[c], z[c], sq[c]);
+        }
+      }
+      if (gram_tile) {
+#pragma unroll
+        for (int c = 0; c < PM8; ++c)
+          sZ[c * kTileStride + threadIdx.x] = (c < PM) ? z[c < PM ? c : 0] : 0.0;
+      }
+    }
+    if (!gram_tile) continue;
+    __syncthreads();
+    // ---------------- phase 2: Gram of this tile on the FP64 tensor cores
+    {
+      constexpr int kSteps = kTallThreads / 4 / kTallWarps;  // k-steps (4 rows) per warp
+      const int kr = lane & 3;   // k index inside the step
+      const int mn = lane >> 2;  // m (A) / n (B) index inside the 8x8 tile
+#pragma unroll 2
+      for (int s = 0; s < kSteps; ++s) {
+        const int r = (w * kSteps + s) * 4 + kr;
+        const int64_t i = tile0 + r;
+        double b[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = sZ[(nt * 8 + mn) * kTileStride + r];
+        double a[MTMAX];
+        if (P.gmode == 1) {
+#pragma unroll
+          for (int mt = 0; mt < MTMAX; ++mt) {
+            const int gg = mt * 8 + mn;
+            a[mt] = (mt < mtiles && gg < P.gc && i < P.n) ? __ldg(P.gb + i + (int64_t)gg * P.ldgb) : 0.0;
+          }
+        } else {
+#pragma unroll
+          for (int mt = 0; mt < MTMAX; ++mt) {
+            const int gg = mt * 8 + mn;
+            a[mt] = (mt < mtiles && gg < PM8) ? sZ[gg * kTileStride + r] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int mt = 0; mt < MTMAX; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+          }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---------------- epilogue: CTA partial -> workspace
+  __shared__ bool s_last;
+  if (gram_tile) {
+    // sum warp fragments in warp order (deterministic)
+    for (int ww = 0; ww < kTallWarps; ++ww) {
+      if (w == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTMAX; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+                sRed[idx] = (ww == 0) ? acc[mt][nt][v] : sRed[idx] + acc[mt][nt][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kTallThreads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mrow = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mrow * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = sRed[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    double* red = sZ;
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[w * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kTallThreads) {
+      double s = 0.0;
+      for (int ww = 0; ww < kTallWarps; ++ww) s += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = s;
+    }
+  }
+  if (P.gmode == 0) return;
+
+  // ---------------- last CTA: deterministic cross-CTA sum
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = (P.gmode == 3) ? p : P.gc * p;
+  for (int e = threadIdx.x; e < ne; e += kTallThreads) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = s;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;  // re-arm for the next launch on this workspace
+}
+
+static int pick_pm(int p) {
+  if (p <= 1) return 1;
+  if (p <= 2) return 2;
+  if (p <= 4) return 4;
+  if (p <= 8) return 8;
+  return 16;
+}
+static int pick_mtmax(int mtiles) {
+  if (mtiles <= 2) return 2;
+  if (mtiles <= 6) return 6;
+  if (mtiles <= 12) return 12;
+  return 16;
+}
+
+static size_t tall_smem(int PM, int a1, int a2, bool r1, bool r2, int gmode, int mtmax) {
+  const int PM8 = PM < 8 ? 8 : PM;
+  size_t words = (size_t)(a1 + a2) * PM + (r1 ? PM * PM : 0) + (r2 ? PM * PM : 0);
+  if (gmode == 1 || gmode == 2)
+    words += (size_t)PM8 * kTileStride + (size_t)mtmax * (PM8 / 8) * 64;
+  else if (gmode == 3)
+    words += (size_t)kTallWarps * PM;
+  return words * sizeof(double);
+}
+
+template <int PM, int MTMAX>
+static cudaError_t launch_tall(const TallParams& P, size_t smem, int64_t max_grid, cudaStream_t st) {
+  auto k = tall_kernel<PM, MTMAX>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kTallThreads, 48 * 1024);
+    per_sm = v < 1 ? 1 : v;
+  }
+  int64_t g = (int64_t)sm_count() * per_sm;
+  if (g > max_grid) g = max_grid;
+  if (P.ntiles < g) g = P.ntiles;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kTallThreads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+// upper bound on the grid of any rg_tall launch (workspace sizing)
+static int64_t tall_grid_bound() { return (int64_t)sm_count() * 2; }
+
+#define RG_TALL_CASE(PMv)                                                                 \
+  case PMv:                                                                               \
+    switch (mtmax) {                                                                      \
+      case 2: e = launch_tall<PMv, 2>(P, smem, bound, st); break;                         \
+      case 6: e = launch_tall<PMv, 6>(P, smem, bound, st); break;                         \
+      case 12: e = launch_tall<PMv, 12>(P, smem, bound, st); break;                       \
+      default: e = launch_tall<PMv, 16>(P, smem, bound, st); break;                       \
+    }                                                                                     \
+    break;
+
+}  // namespace rg
+
+extern "C" int64_t rg_tall_workspace_bytes(int64_t n, int32_t p, int32_t a1, int32_t a2,
+                                           int32_t gram_mode, int32_t gc) {
+  (void)n; (void)a1; (void)a2;
+  using namespace rg;
+  int64_t ne = 0;
+  if (gram_mode == 1) ne = (int64_t)gc * p;
+  if (gram_mode == 2) ne = (int64_t)p * p;
+  if (gram_mode == 3) ne = p;
+  return 256 + tall_grid_bound() * ne * (int64_t)sizeof(double);
+}
+
+extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ldzin,
+                           double* d_zout, int64_t ldzout, const double* d_x1, int64_t ldx1,
+                           int32_t a1, const double* d_s1, double alpha1, const double* d_x2,
+                           int64_t ldx2, int32_t a2, const double* d_s2, double alpha2,
+                           const double* d_r1, const double* d_r2, int32_t gram_mode,
+                           const double* d_gb, int64_t ldgb, int32_t gc, double* d_gout,
+                           void* d_work, int64_t work_bytes, void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n >= 0, "rg_tall_f64: n=%lld < 0", (long long)n);
+  RG_REQUIRE(p >= 1 && p <= 16, "rg_tall_f64: block width p=%d outside [1, 16]", p);
+  RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= 512, "rg_tall_f64: term widths %d, %d", a1, a2);
+  RG_REQUIRE(!d_zin || ldzin >= n, "rg_tall_f64: ldzin < n");
+  RG_REQUIRE(!d_zout || ldzout >= n, "rg_tall_f64: ldzout < n");
+  RG_REQUIRE(a1 == 0 || (d_x1 && d_s1 && ldx1 >= n), "rg_tall_f64: bad term 1");
+  RG_REQUIRE(a2 == 0 || (d_x2 && d_s2 && ldx2 >= n), "rg_tall_f64: bad term 2");
+  RG_REQUIRE(gram_mode >= 0 && gram_mode <= 3, "rg_tall_f64: gram_mode %d", gram_mode);
+  RG_REQUIRE(gram_mode != 1 || (d_gb && gc >= 1 && gc <= 128 && ldgb >= n),
+             "rg_tall_f64: Gram basis must be n x gc with 1 <= gc <= 128 (gc=%d)", gc);
+  RG_REQUIRE(gram_mode != 2 || gc == p, "rg_tall_f64: self Gram needs gc == p");
+  RG_REQUIRE(gram_mode == 0 || d_gout, "rg_tall_f64: null Gram output");
+  if (gram_mode == 3) gc = 1;
+  const int64_t need = rg_tall_workspace_bytes(n, p, a1, a2, gram_mode, gc);
+  RG_REQUIRE(gram_mode == 0 || (d_work && work_bytes >= need),
+             "rg_tall_f64: workspace %lld bytes < %lld", (long long)work_bytes, (long long)need);
+
+  TallParams P;
+  P.n = n; P.p = p;
+  P.zin = d_zin; P.ldzin = ldzin; P.zout = d_zout; P.ldzout = ldzout;
+  P.x1 = d_x1; P.ldx1 = ldx1; P.a1 = a1; P.s1 = d_s1; P.alpha1 = alpha1;
+  P.x2 = d_x2; P.ldx2 = ldx2; P.a2 = a2; P.s2 = d_s2; P.alpha2 = alpha2;
+  P.r1 = d_r1; P.r2 = d_r2;
+  P.gmode = gram_mode; P.gb = d_gb; P.ldgb = ldgb; P.gc = gc; P.gout = d_gout;
+  P.mtiles = (gram_mode == 1 || gram_mode == 2) ? (gc + 7) / 8 : 0;
+  P.counter = (unsigned int*)d_work;
+  P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
+  P.ntiles = (n + kTallThreads - 1) / kTallThreads;
+  if (gram_mode == 0 && P.ntiles == 0) return RG_OK;
+  const int PM = pick_pm(p);
+  const int mtmax = pick_mtmax(P.mtiles);
+  const size_t smem = tall_smem(PM, a1, a2, d_r1 != nullptr, d_r2 != nullptr, gram_mode, mtmax);
+  RG_REQUIRE(smem <= 200 * 1024, "rg_tall_f64: %zu bytes of shared memory (terms too wide)", smem);
+  const int64_t bound = tall_grid_bound();
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  switch (PM) {
+    RG_TALL_CASE(1)
+    RG_TALL_CASE(2)
+    RG_TALL_CASE(4)
+    RG_TALL_CASE(8)
+    RG_TALL_CASE(16)
+  }
+  if (e != cudaSuccess) {
+    set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+    return RG_ECUDA;
+  }
+  return RG_OK;
+}

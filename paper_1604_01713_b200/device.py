@@ -1,0 +1,416 @@
+"""Device-side plumbing: column-major blocks in HBM, workspace, and the thin
+wrappers that launch librgb200 kernels on torch's current CUDA stream.
+
+Layout: every n x p block is column-major (Fortran order,
+like the reference's ``as_block``, sparse_core.py:51-58) with a leading
+dimension ``ld`` rounded up to a multiple of 32 doubles (256 B), so every
+column starts on a 256-byte boundary and warp accesses are full segments.
+torch is used only as the allocator / stream provider.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+
+LD_ALIGN = 32
+MAX_P = 16        # block width one rg_tall launch handles
+MAX_GC = 128      # Gram basis columns per launch
+MAX_TERM_COLS = 512
+
+
+class NoDeviceError(RuntimeError):
+    """The B200 path needs a CUDA device; there is no CPU fallback."""
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise NoDeviceError("paper_1604_01713_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise NoDeviceError(f"device {dev} is not a CUDA device")
+    return dev
+
+
+def lib():
+    return _lib.load()
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def round_ld(n: int) -> int:
+    return max(LD_ALIGN, (int(n) + LD_ALIGN - 1) // LD_ALIGN * LD_ALIGN)
+
+
+def empty_block(n: int, p: int, device=None, dtype=torch.float64, ld: int | None = None) -> torch.Tensor:
+    """Column-major (n, p) tensor with padded leading dimension."""
+    dev = require_cuda(device)
+    ld = round_ld(n) if ld is None else ld
+    store = torch.empty((max(p, 1), ld), dtype=dtype, device=dev)
+    return store.t()[:n, :p]
+
+
+def zeros_block(n: int, p: int, device=None, dtype=torch.float64) -> torch.Tensor:
+    b = empty_block(n, p, device, dtype)
+    b.zero_()
+    return b
+
+
+def small(rows: int, cols: int, device=None, dtype=torch.float64) -> torch.Tensor:
+    """Dense column-major rows x cols with ld = rows (coefficient matrices)."""
+    dev = require_cuda(device)
+    return torch.empty((max(cols, 1), max(rows, 1)), dtype=dtype, device=dev).t()[:rows, :cols]
+
+
+def ld_of(t: torch.Tensor) -> int:
+    n = t.shape[0]
+    if t.dim() == 1:
+        return max(n, 1)
+    if t.shape[1] <= 1:
+        s = t.stride(1)
+        return s if s >= n else max(n, 1)
+    return t.stride(1)
+
+
+def is_col_major(t: torch.Tensor) -> bool:
+    if t.dim() != 2:
+        return False
+    if t.shape[0] > 1 and t.stride(0) != 1:
+        return False
+    return t.shape[1] <= 1 or t.stride(1) >= t.shape[0]
+
+
+def to_device_block(x, device=None, dtype=torch.float64) -> torch.Tensor:
+    """numpy / torch 2-D input -> column-major CUDA tensor (copies if needed)."""
+    dev = require_cuda(device)
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.dim() == 1:
+            t = t.reshape(-1, 1)
+        if t.device == dev and t.dtype == dtype and is_col_major(t):
+            return t
+        out = empty_block(t.shape[0], t.shape[1], dev, dtype)
+        out.copy_(t)
+        return out
+    a = np.asarray(x)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    np_dtype = np.complex128 if dtype == torch.complex128 else np.float64
+    a = np.asfortranarray(a, dtype=np_dtype)
+    out = empty_block(a.shape[0], a.shape[1], dev, dtype)
+    # a is F-ordered: its transpose is a C-contiguous (p, n) array
+    out.copy_(torch.from_numpy(a.T).t())
+    return out
+
+
+def to_numpy_block(t: torch.Tensor) -> np.ndarray:
+    """Column-major CUDA block -> Fortran-ordered numpy array (D2H)."""
+    host = t.t().contiguous().cpu().numpy()  # (p, n) C-order
+    return np.asfortranarray(host.T)
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+class Workspace:
+    """Per-device scratch buffer; the leading 256 bytes hold the ticket
+    counter of rg_tall's last-CTA reduction (zeroed once, re-armed by the
+    kernels)."""
+
+    _pools: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device=None, slot: int = 0) -> torch.Tensor:
+        dev = require_cuda(device)
+        key = (dev.index, slot)
+        buf = cls._pools.get(key)
+        if buf is None or buf.numel() < nbytes:
+            size = max(int(nbytes), 1 << 20)
+            if buf is not None:
+                size = max(size, 2 * buf.numel())
+                torch.cuda.current_stream(dev).synchronize()
+            buf = torch.zeros(size, dtype=torch.uint8, device=dev)
+            cls._pools[key] = buf
+        return buf
+
+
+# ---------------------------------------------------------------------------
+# launch accounting (bench / smoke evidence): every rg_* launch is counted;
+# with ``timing`` on, each wrapper call is bracketed by CUDA events on the
+# launching stream together with its algorithmic byte count.
+# ---------------------------------------------------------------------------
+
+
+class LaunchLog:
+    count = 0
+    timing = False
+    records: list = []
+
+    @classmethod
+    def reset(cls, timing: bool = False):
+        cls.count = 0
+        cls.timing = timing
+        cls.records = []
+
+    @classmethod
+    def summary(cls):
+        """{label: (calls, total_ms, total_bytes)} (synchronises)."""
+        torch.cuda.synchronize()
+        out = {}
+        for label, nbytes, e0, e1 in cls.records:
+            c, t, b = out.get(label, (0, 0.0, 0))
+            out[label] = (c + 1, t + e0.elapsed_time(e1), b + nbytes)
+        return out
+
+
+def _t0():
+    if not LaunchLog.timing:
+        return None
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _t1(e0, label, nbytes, nlaunch=1):
+    LaunchLog.count += nlaunch
+    if e0 is not None:
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record()
+        LaunchLog.records.append((label, int(nbytes), e0, e1))
+
+
+# ---------------------------------------------------------------------------
+# kernel wrappers
+# ---------------------------------------------------------------------------
+
+
+def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: int | None = None,
+         n_local: int | None = None, Xg: torch.Tensor | None = None) -> torch.Tensor:
+    """Y[rows] = A[rows] @ X (bitwise the reference kernel's arithmetic)."""
+    L = lib()
+    n_rows = dcsr.n_rows
+    row_end = n_rows if row_end is None else row_end
+    p = X.shape[1]
+    n_local = dcsr.n_cols if n_local is None else n_local
+    cplx = X.dtype == torch.complex128
+    fn = L.rg_spmm_csr_c128 if cplx else L.rg_spmm_csr_f64
+    e0 = _t0()
+    rc = fn(n_rows, row_begin, row_end, dcsr.row_ptr.data_ptr(), dcsr.col_idx.data_ptr(),
+            dcsr.values.data_ptr(), X.data_ptr() if X.numel() else None, ld_of(X), n_local,
+            ptr(Xg), ld_of(Xg) if Xg is not None else 1, p, Y.data_ptr(), ld_of(Y), stream_ptr())
+    _lib.check(rc, "spmm")
+    rows = row_end - row_begin
+    if rows > 0:
+        esz = 16 if cplx else 8
+        hrp = getattr(dcsr, "host_row_ptr", None)
+        nnz = int(hrp[row_end] - hrp[row_begin]) if hrp is not None else 0
+        _t1(e0, f"rg_spmm p={p}", nnz * (esz + 4) + (rows + 1) * 4 + 2 * p * rows * esz, (p + 15) // 16)
+    return Y
+
+
+def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
+    L = lib()
+    x1, s1, al1 = t1 if t1 is not None else (None, None, 0.0)
+    x2, s2, al2 = t2 if t2 is not None else (None, None, 0.0)
+    a1 = 0 if x1 is None else x1.shape[1]
+    a2 = 0 if x2 is None else x2.shape[1]
+    gc = 0
+    if gmode == 1:
+        gc = gb.shape[1]
+    elif gmode == 2:
+        gc = p
+    elif gmode == 3:
+        gc = 1
+    gout_k = gout
+    if gout is not None and not _dense_f(gout):
+        gout_k = small(gout.shape[0], gout.shape[1] if gout.dim() > 1 else 1, gout.device, gout.dtype)
+        if gout.dim() == 1:
+            gout_k = gout_k[:, 0]
+    wsfn = L.rg_tall_c128_workspace_bytes if cplx else L.rg_tall_workspace_bytes
+    wsb = wsfn(n, p, a1, a2, gmode, gc) if gmode else 0
+    ws = Workspace.get(wsb) if gmode else None
+    fn = L.rg_tall_c128 if cplx else L.rg_tall_f64
+    e0 = _t0()
+    rc = fn(n, p,
+            ptr(zin), ld_of(zin) if zin is not None else 1,
+            ptr(zout), ld_of(zout) if zout is not None else 1,
+            ptr(x1), ld_of(x1) if x1 is not None else 1, a1, ptr(s1), float(al1),
+            ptr(x2), ld_of(x2) if x2 is not None else 1, a2, ptr(s2), float(al2),
+            ptr(r1), ptr(r2), gmode,
+            ptr(gb), ld_of(gb) if gb is not None else 1, gc, ptr(gout_k),
+            ptr(ws), ws.numel() if ws is not None else 0, stream_ptr())
+    _lib.check(rc, "tall")
+    if n > 0 or gmode:
+        esz = 16 if cplx else 8
+        cols = (p if zin is not None else 0) + a1 + a2 + (gc if gmode == 1 else 0) + (p if zout is not None else 0)
+        label = (f"rg_tall p={p} in={int(zin is not None)} a={a1}+{a2} "
+                 f"g{gmode}:{gc} trsm={int(r1 is not None) + int(r2 is not None)} out={int(zout is not None)}")
+        _t1(e0, label, esz * n * cols)
+    if gout_k is not gout:
+        gout.copy_(gout_k)
+
+
+def _dense_f(t: torch.Tensor) -> bool:
+    if t.dim() == 1:
+        return t.stride(0) == 1 or t.shape[0] <= 1
+    return (t.shape[0] <= 1 or t.stride(0) == 1) and (t.shape[1] <= 1 or t.stride(1) == t.shape[0])
+
+
+def _coef(S: torch.Tensor) -> torch.Tensor:
+    """Coefficient matrices must be dense column-major with ld = rows."""
+    if S.dim() == 1:
+        S = S.reshape(-1, 1)
+    a, p = S.shape
+    if S.stride(0) == 1 and (p <= 1 or S.stride(1) == a):
+        return S
+    out = small(a, p, S.device, S.dtype)
+    out.copy_(S)
+    return out
+
+
+def _split_terms(terms):
+    """Split wide terms so that each launch stages <= MAX_TERM_COLS columns."""
+    pieces = []
+    for X, S, alpha in terms:
+        a = X.shape[1]
+        if a == 0:
+            continue
+        for a0 in range(0, a, MAX_TERM_COLS):
+            a1 = min(a, a0 + MAX_TERM_COLS)
+            pieces.append((X[:, a0:a1], _coef(S[a0:a1, :]), alpha))
+    return pieces
+
+
+def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=None, r2=None,
+         gram=None, n: int | None = None, p: int | None = None):
+    """Fused pass ``z = Zin + sum alpha_t X_t S_t; z = z R1^-1 R2^-1;
+    Zout = z; Gram``.  ``gram`` is None, ("basis", Gb, Gout), ("self", Gout)
+    or ("sumsq", out).  Shapes beyond one launch are split into several
+    passes (wide term lists, Gram bases wider than 128 columns, block widths
+    above 16); the split changes only the rounding order.
+    """
+    if n is None:
+        n = (Z_in if Z_in is not None else Z_out).shape[0]
+    if p is None:
+        p = (Z_in if Z_in is not None else Z_out).shape[1]
+    if n == 0 and gram is not None:
+        _zero_gram(gram)
+        return
+    cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
+    terms = _split_terms(terms)
+    r1 = _coef(r1) if r1 is not None else None
+    r2 = _coef(r2) if r2 is not None else None
+    if p > MAX_P:
+        _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx)
+        return
+    gmode, gb, gout = 0, None, None
+    if gram is not None:
+        kind = gram[0]
+        if kind == "basis":
+            gmode, gb, gout = 1, gram[1], gram[2]
+        elif kind == "self":
+            gmode, gout = 2, gram[1]
+        elif kind == "sumsq":
+            gmode, gout = 3, gram[1]
+        else:
+            raise ValueError(f"unknown gram kind {kind!r}")
+    # passes over the term list (<= 2 terms each)
+    groups = [terms[i:i + 2] for i in range(0, len(terms), 2)] or [[]]
+    needs_multi = len(groups) > 1 or (gmode == 1 and gb.shape[1] > MAX_GC)
+    zbuf = Z_out
+    if needs_multi and zbuf is None:
+        zbuf = empty_block(n, p, Z_in.device if Z_in is not None else None,
+                           torch.complex128 if cplx else torch.float64)
+    cur_in = Z_in
+    for gi, grp in enumerate(groups):
+        last = gi == len(groups) - 1
+        t1 = grp[0] if len(grp) > 0 else None
+        t2 = grp[1] if len(grp) > 1 else None
+        if not last:
+            _tall_call(n, p, cur_in, zbuf, t1, t2, None, None, 0, None, None, cplx)
+            cur_in = zbuf
+            continue
+        if gmode == 1 and gb.shape[1] > MAX_GC:
+            gc = gb.shape[1]
+            _tall_call(n, p, cur_in, zbuf, t1, t2, r1, r2, 1, gb[:, :MAX_GC], gout[:MAX_GC, :], cplx)
+            for g0 in range(MAX_GC, gc, MAX_GC):
+                g1 = min(gc, g0 + MAX_GC)
+                _tall_call(n, p, zbuf, None, None, None, None, None, 1, gb[:, g0:g1], gout[g0:g1, :], cplx)
+        else:
+            _tall_call(n, p, cur_in, zbuf if needs_multi else Z_out, t1, t2, r1, r2, gmode, gb, gout, cplx)
+
+
+def _zero_gram(gram):
+    kind = gram[0]
+    out = gram[2] if kind == "basis" else gram[1]
+    out.zero_()
+
+
+def _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx):
+    """p > 16: column-blocked passes (materialise z, blocked triangular
+    solves, blocked Grams)."""
+    dev = (Z_in if Z_in is not None else Z_out).device
+    dt = torch.complex128 if cplx else torch.float64
+    Z = Z_out if Z_out is not None else empty_block(n, p, dev, dt)
+    blocks = [(c0, min(p, c0 + MAX_P)) for c0 in range(0, p, MAX_P)]
+    # 1) z = Zin + terms, column block by column block
+    for c0, c1 in blocks:
+        sub_terms = [(X, S[:, c0:c1], al) for X, S, al in terms]
+        tall(Z_in[:, c0:c1] if Z_in is not None else None, Z[:, c0:c1], sub_terms, n=n, p=c1 - c0)
+    # 2) right triangular solves, block forward substitution
+    for R in (r1, r2):
+        if R is None:
+            continue
+        for bi, (c0, c1) in enumerate(blocks):
+            prev = [(Z[:, b0:b1], R[b0:b1, c0:c1], -1.0) for b0, b1 in blocks[:bi]]
+            tall(Z[:, c0:c1], Z[:, c0:c1], prev, r1=R[c0:c1, c0:c1], n=n, p=c1 - c0)
+    # 3) Gram
+    if gram is None:
+        return
+    kind = gram[0]
+    for c0, c1 in blocks:
+        zc = Z[:, c0:c1]
+        if kind == "basis":
+            gb, gout = gram[1], gram[2]
+            tall(zc, None, gram=("basis", gb, gout[:, c0:c1]), n=n, p=c1 - c0)
+        elif kind == "self":
+            gout = gram[1]
+            tall(zc, None, gram=("basis", Z, gout[:, c0:c1]), n=n, p=c1 - c0)
+        else:
+            tall(zc, None, gram=("sumsq", gram[1][c0:c1]), n=n, p=c1 - c0)
+
+
+def chol(G: torch.Tensor, R: torch.Tensor, status: torch.Tensor, cond_tol: float):
+    p = G.shape[0]
+    e0 = _t0()
+    rc = lib().rg_chol_f64(p, _coef(G).data_ptr(), R.data_ptr(), status.data_ptr(), float(cond_tol), stream_ptr())
+    _lib.check(rc, "chol")
+    _t1(e0, "rg_chol", 0)
+
+
+def tsqr(X: torch.Tensor, R: torch.Tensor):
+    """In-place Householder TSQR: X <- Q, R <- R (r_jj >= 0)."""
+    n, p = X.shape
+    L = lib()
+    wsb = L.rg_tsqr_workspace_bytes(n, p)
+    ws = Workspace.get(wsb, slot=1)
+    e0 = _t0()
+    rc = L.rg_tsqr_f64(n, p, X.data_ptr(), ld_of(X), R.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check(rc, "tsqr")
+    _t1(e0, f"rg_tsqr p={p}", 3 * 8 * n * p, 1 + 2 * _tsqr_levels(n, p))
+
+
+def _tsqr_levels(n, p):
+    c = 1024 if p <= 8 else (512 if p <= 16 else 256)
+    lv, m = 1, n
+    while (m + c - 1) // c > 1:
+        m = ((m + c - 1) // c) * p
+        lv += 1
+    return lv

@@ -1,0 +1,233 @@
+"""GPU parity of the librgb200 kernels against the oracle and the golden
+vectors of the reference (bitwise for SpMM, 1e-12 relative for the FP64
+dense kernels)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import csr_from, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev():
+    from paper_1604_01713_b200 import device as D
+
+    return D
+
+
+# ---------------------------------------------------------------- SpMM (K1)
+
+
+def test_spmm_golden_bitwise(cuda):
+    from paper_1604_01713_b200.sparse_core import CsrMatrix, spmm
+
+    g = load_golden("spmm_cases.npz")
+    for name in g["cases"]:
+        rp, ci, v, shape = csr_from(g, f"{name}/")
+        A = CsrMatrix(shape[0], shape[1], rp, ci, v)
+        Y = spmm(A, g[f"{name}/X"])
+        assert Y.flags.f_contiguous
+        assert np.array_equal(Y, g[f"{name}/Y"]), f"{name}: SpMM differs from the reference bitwise"
+
+
+def test_spmm_device_tensor_roundtrip(cuda):
+    from paper_1604_01713_b200 import problems
+    from paper_1604_01713_b200.sparse_core import spmm
+
+    A = problems.conv_diff_2d(20, 10.0)
+    X = np.random.default_rng(0).standard_normal((A.n_rows, 3))
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).to(cuda)  # row-major input gets converted
+    Yd = spmm(A, Xd)
+    assert isinstance(Yd, torch.Tensor) and Yd.is_cuda
+    assert np.array_equal(Yd.cpu().numpy(), oracle.spmm(A.row_ptr, A.col_idx, A.values, X))
+
+
+@pytest.mark.parametrize("p", [1, 2, 4, 8, 16])
+def test_spmm_cfg2_full_size_bitwise(cuda, p):
+    """BASELINE configs[1]: 128^3 7-point Laplacian, V ~ N(0,1) n x p."""
+    from paper_1604_01713_b200 import problems
+    from paper_1604_01713_b200.sparse_core import spmm_device
+
+    A = problems.laplacian_3d(128)
+    assert (A.n_rows, A.nnz) == (2097152, 14581760)
+    V = np.asfortranarray(np.random.default_rng(0).standard_normal((A.n_rows, p)))
+    Y = spmm_device(A, _dev().to_device_block(V))
+    ref = oracle.spmm(A.row_ptr, A.col_idx, A.values, V)
+    assert np.array_equal(_dev().to_numpy_block(Y), ref)
+
+
+def test_spmm_row_range_and_ghosts(cuda):
+    """Row-range launches and the ghost-column path used by the row
+    partition reproduce the single launch bitwise."""
+    from paper_1604_01713_b200 import problems
+    from paper_1604_01713_b200.sparse_core import spmm_device
+
+    D = _dev()
+    A = problems.laplacian_3d(12)
+    n = A.n_rows
+    X = np.random.default_rng(1).standard_normal((n, 5))
+    ref = oracle.spmm(A.row_ptr, A.col_idx, A.values, X)
+    dA = A.device()
+    Xd = D.to_device_block(X)
+    Y = D.zeros_block(n, 5)
+    D.spmm(dA, Xd, Y, 0, 700)
+    D.spmm(dA, Xd, Y, 700, n)
+    assert np.array_equal(D.to_numpy_block(Y), ref)
+    # ghost path: columns >= n_local come from a separate buffer
+    half = n // 2
+    Xg = D.to_device_block(X[half:])
+    Y2 = D.zeros_block(n, 5)
+    D.spmm(dA, D.to_device_block(X[:half]), Y2, 0, n, n_local=half, Xg=Xg)
+    assert np.array_equal(D.to_numpy_block(Y2), ref)
+
+
+def test_spmm_shape_error(cuda):
+    from paper_1604_01713_b200 import CsrMatrix, ShapeError, spmm
+
+    A = CsrMatrix.from_coo(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0])
+    with pytest.raises(ShapeError):
+        spmm(A, np.ones((4, 2)))
+
+
+# ---------------------------------------------------------------- tall-skinny passes (K2/K3/K6/K7)
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+@pytest.mark.parametrize("n", [1, 255, 256, 1000, 100003])
+@pytest.mark.parametrize("p", [1, 3, 8, 16])
+def test_tall_gram_and_update(cuda, n, p):
+    D = _dev()
+    rng = np.random.default_rng(n + p)
+    for gc in (1, 7, 20, 80, 130):
+        Gb = rng.standard_normal((n, gc))
+        Z = rng.standard_normal((n, p))
+        out = D.small(gc, p)
+        D.tall(D.to_device_block(Z), None, gram=("basis", D.to_device_block(Gb), out))
+        assert _rel(out.cpu().numpy(), Gb.T @ Z) <= 1e-12
+    X1 = rng.standard_normal((n, 20))
+    S1 = rng.standard_normal((20, p))
+    X2 = rng.standard_normal((n, 37))
+    S2 = rng.standard_normal((37, p))
+    Z = rng.standard_normal((n, p))
+    Zd = D.to_device_block(Z)
+    Zo = D.empty_block(n, p)
+    G = D.small(p, p)
+    D.tall(Zd, Zo, [(D.to_device_block(X1), torch.from_numpy(S1).to(cuda), -1.0),
+                    (D.to_device_block(X2), torch.from_numpy(S2).to(cuda), -1.0)], gram=("self", G))
+    ref = (Z - X1 @ S1) - X2 @ S2
+    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
+    assert _rel(G.cpu().numpy(), ref.T @ ref) <= 1e-12
+    ss = torch.zeros(p, dtype=torch.float64, device=cuda)
+    D.tall(Zo, None, gram=("sumsq", ss))
+    assert _rel(ss.cpu().numpy(), (ref * ref).sum(axis=0)) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [1, 4, 8, 16, 20, 32])
+def test_tall_trsm(cuda, p):
+    D = _dev()
+    rng = np.random.default_rng(p)
+    n = 5000
+    Z = rng.standard_normal((n, p))
+    R1 = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
+    R2 = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
+    Zo = D.empty_block(n, p)
+    D.tall(D.to_device_block(Z), Zo, r1=torch.from_numpy(R1).to(cuda), r2=torch.from_numpy(R2).to(cuda))
+    ref = np.linalg.solve(R2.T, np.linalg.solve(R1.T, Z.T)).T
+    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
+
+
+def test_tall_wide_terms_and_gram_split(cuda):
+    """term lists longer than 2, basis wider than 128 columns, p > 16."""
+    D = _dev()
+    rng = np.random.default_rng(9)
+    n, p = 3000, 20
+    Xs = [rng.standard_normal((n, a)) for a in (5, 9, 600)]
+    Ss = [rng.standard_normal((a, p)) for a in (5, 9, 600)]
+    Z = rng.standard_normal((n, p))
+    Gb = rng.standard_normal((n, 300))
+    Zo = D.empty_block(n, p)
+    out = D.small(300, p)
+    D.tall(D.to_device_block(Z), Zo, [(D.to_device_block(X), torch.from_numpy(S).to(cuda), -1.0)
+                                      for X, S in zip(Xs, Ss)], gram=("basis", D.to_device_block(Gb), out))
+    ref = Z.copy()
+    for X, S in zip(Xs, Ss):
+        ref = ref - X @ S
+    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-11
+    assert _rel(out.cpu().numpy(), Gb.T @ ref) <= 1e-11
+
+
+def test_tall_empty_rows(cuda):
+    D = _dev()
+    out = D.small(3, 2)
+    out.fill_(7.0)
+    D.tall(D.empty_block(0, 2), None, gram=("basis", D.empty_block(0, 3), out))
+    assert np.all(out.cpu().numpy() == 0.0)
+
+
+def test_tall_deterministic(cuda):
+    D = _dev()
+    rng = np.random.default_rng(3)
+    n, p = 1_000_003, 8
+    Zd = D.to_device_block(rng.standard_normal((n, p)))
+    Wd = D.to_device_block(rng.standard_normal((n, 80)))
+    outs = []
+    for _ in range(3):
+        o = D.small(80, p)
+        D.tall(Zd, None, gram=("basis", Wd, o))
+        outs.append(o.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
+
+
+# ---------------------------------------------------------------- QR (K5)
+
+
+def test_reduced_qr_golden(cuda):
+    from paper_1604_01713_b200.dense_kernels import reduced_qr
+
+    g = load_golden("qr_cases.npz")
+    for name in g["cases"]:
+        X = g[f"{name}/X"]
+        f = reduced_qr(X)
+        r_ref = g[f"{name}/r"]
+        flagged = g[f"{name}/flagged"]
+        assert f.flagged.tolist() == flagged.tolist(), name
+        assert f.rank == int(g[f"{name}/rank"]), name
+        cond = np.linalg.cond(X) if not flagged.any() else 1.0
+        ok = ~flagged
+        tol = 1e-12 * max(cond, 1.0) * max(np.abs(r_ref).max(), 1.0)
+        # R rows of flagged columns are rounding noise in both implementations
+        assert np.abs(f.r_factor[np.ix_(ok, ok)] - r_ref[np.ix_(ok, ok)]).max() <= tol, name
+        assert np.all(np.diagonal(f.r_factor) >= 0.0)
+        q = f.q
+        assert np.abs(q[:, ok] - g[f"{name}/q"][:, ok]).max() <= 1e-12 * max(cond, 1.0) * 10, name
+        assert np.linalg.norm(q.T @ q - np.eye(q.shape[1])) <= 1e-12 * q.shape[1]
+
+
+def test_reduced_qr_rejects_wide(cuda):
+    from paper_1604_01713_b200.dense_kernels import reduced_qr
+
+    with pytest.raises(ValueError):
+        reduced_qr(np.ones((2, 3)))
+
+
+@pytest.mark.parametrize("p", [1, 8, 16, 20, 32])
+def test_tsqr_large(cuda, p):
+    D = _dev()
+    rng = np.random.default_rng(p)
+    n = 300_001
+    X = rng.standard_normal((n, p)) * np.logspace(0, -3, p)
+    Q = D.to_device_block(X)
+    R = D.small(p, p)
+    D.tsqr(Q, R)
+    q_ref, r_ref, _ = oracle.reduced_qr(X)
+    Rh = np.triu(R.cpu().numpy())
+    assert _rel(Rh, r_ref) <= 1e-12 * np.linalg.cond(X)
+    Qh = D.to_numpy_block(Q)
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(p)) <= 1e-13 * p
+    assert np.linalg.norm(Qh @ Rh - X) <= 1e-13 * np.linalg.norm(X)

@@ -1,0 +1,173 @@
+"""GPU parity of the device-resident Arnoldi process, recycle-space algebra
+and the block GCRO-DR drivers against golden runs of the reference."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import csr_matrix_from, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _fact_from(W, H, F, m, L, k, device):
+    from paper_1604_01713_b200 import device as D
+    from paper_1604_01713_b200.arnoldi import ArnoldiFactorization
+
+    n = W.shape[0]
+    fact = ArnoldiFactorization(n, L, m, k, 1e-12, 0, device)
+    fact._W[:, : W.shape[1]].copy_(D.to_device_block(W))
+    fact._H[: H.shape[0], : H.shape[1]] = H
+    if k:
+        fact._F[:, : F.shape[1]] = F
+    fact.m = m
+    return fact
+
+
+def test_arnoldi_golden(cuda):
+    from paper_1604_01713_b200 import arnoldi
+    from paper_1604_01713_b200.recycling import RecycleSpace
+    from paper_1604_01713_b200.solver import _Operator
+
+    g = load_golden("arnoldi_cases.npz")
+    for name in g["cases"]:
+        A = csr_matrix_from(g, f"{name}/")
+        m, k, seed = int(g[f"{name}/m"]), int(g[f"{name}/k"]), int(g[f"{name}/seed"])
+        rs = RecycleSpace(u=g[f"{name}/U"], c=g[f"{name}/C"]) if k else None
+        op = _Operator(A, None, "none")
+        fact = arnoldi.start(op.apply, g[f"{name}/R0"], m_max=m, recycle=rs, seed=seed)
+        for _ in range(m):
+            arnoldi.step(fact, op.apply, recycle=rs)
+        scale = A.frobenius_norm()
+        assert np.abs(fact.h_bar - g[f"{name}/H"]).max() <= 1e-10 * scale, name
+        assert np.abs(fact.z_bar - g[f"{name}/z_bar"]).max() <= 1e-12 * np.abs(g[f"{name}/z_bar"]).max(), name
+        if k:
+            assert np.abs(fact.f - g[f"{name}/F"]).max() <= 1e-10 * scale, name
+        assert np.abs(fact.w_numpy() - g[f"{name}/W"]).max() <= 1e-9, name
+        assert len(fact.breakdown_events) == int(g[f"{name}/events"]), name
+        # exact block-Hessenberg zeros and nonnegative closing diagonals
+        H, L = fact.h_bar, fact.L
+        for j in range(m):
+            assert np.all(H[(j + 2) * L:, j * L:(j + 1) * L] == 0.0)
+            assert np.all(np.diagonal(H[(j + 1) * L:(j + 2) * L, j * L:(j + 1) * L]) >= 0.0)
+
+
+def test_arnoldi_invariants_cfg4_shape(cuda):
+    """Criterion-1 style invariants on a reduced cfg4 grid (32^3 conv-diff,
+    p=8, k=20, m=10): orthonormality, C-orthogonality, Arnoldi relation,
+    F = C^T A W."""
+    from paper_1604_01713_b200 import arnoldi, problems
+    from paper_1604_01713_b200 import device as D
+    from paper_1604_01713_b200.recycling import RecycleSpace, prepare_cross_system
+    from paper_1604_01713_b200.solver import _Operator
+
+    A = problems.conv_diff_3d(32, 20.0)
+    n, L, k, m = A.n_rows, 8, 20, 10
+    rng = np.random.default_rng(0)
+    op = _Operator(A, None, "none")
+    rs = prepare_cross_system(RecycleSpace(u=rng.standard_normal((n, k)), c=None), op.apply)
+    U, C = rs.numpy()
+    assert np.linalg.norm(C.T @ C - np.eye(k)) <= 1e-12 * k
+    AU = A.to_scipy() @ U
+    assert np.linalg.norm(AU - C) <= 1e-10 * np.linalg.norm(AU)
+    R0 = rng.standard_normal((n, L))
+    R0 -= C @ (C.T @ R0)
+    fact = arnoldi.start(op.apply, R0, m_max=m, recycle=rs, seed=0)
+    for _ in range(m):
+        arnoldi.step(fact, op.apply, recycle=rs)
+    W = fact.w_numpy()
+    Ad = A.to_scipy()
+    normA = A.frobenius_norm()
+    assert np.linalg.norm(W.T @ W - np.eye((m + 1) * L)) <= 1e-12 * (m + 1) * L
+    assert np.linalg.norm(C.T @ W) <= 1e-10
+    AW = Ad @ W[:, : m * L]
+    PAW = AW - C @ (C.T @ AW)
+    assert np.linalg.norm(PAW - W @ fact.h_bar) <= 1e-10 * normA
+    assert np.linalg.norm(fact.f - C.T @ AW) <= 1e-10 * normA
+
+
+def _compare_report(rep, g, prefix, bnorm, hist_tol=1e-9):
+    assert rep.cycles == int(g[prefix + "cycles"]), prefix
+    assert [len(h) for h in rep.residual_history] == g[prefix + "steps"].tolist(), prefix
+    assert rep.matvec_count == int(g[prefix + "matvecs"]), prefix
+    assert rep.converged == bool(g[prefix + "converged"]), prefix
+    hist = np.concatenate(rep.residual_history, axis=0)
+    assert np.abs(hist - g[prefix + "hist"]).max() <= hist_tol * bnorm, prefix
+    assert np.abs(np.array(rep.cycle_true_residuals) - g[prefix + "true"]).max() <= hist_tol * bnorm, prefix
+    assert rep.recycle_origin == str(g[prefix + "origin"]), prefix
+
+
+def test_cfg1_sequence_matches_reference(cuda):
+    """BASELINE configs[0]: identical cycles / steps / matvecs, residual
+    histories within 1e-9 ||B||_F (SURVEY.md §8d parity criteria)."""
+    from paper_1604_01713_b200 import SolverConfig, problems, solve_sequence
+
+    g = load_golden("solver_cases.npz")
+    systems, kw = problems.cfg1_sequence()
+    for i, (A, B) in enumerate(systems):
+        ref = csr_matrix_from(g, f"cfg1/A{i}/")
+        assert np.array_equal(A.values, ref.values) and np.array_equal(A.col_idx, ref.col_idx)
+        assert np.array_equal(B, g["cfg1/B"])
+    reps = solve_sequence(systems, SolverConfig(**kw))
+    bnorm = np.linalg.norm(g["cfg1/B"])
+    for i, rep in enumerate(reps):
+        assert rep.error is None, rep.error
+        _compare_report(rep, g, f"cfg1/sys{i}/", bnorm)
+        assert np.abs(rep.solution - g[f"cfg1/sys{i}/X"]).max() <= 1e-6 * np.abs(g[f"cfg1/sys{i}/X"]).max()
+
+
+def test_small_driver_paths(cuda):
+    from paper_1604_01713_b200 import SolverConfig, solve_block_gcrodr, solve_block_gmres
+
+    g = load_golden("solver_cases.npz")
+    A = csr_matrix_from(g, "small/A/")
+    B = g["small/B"]
+    bnorm = np.linalg.norm(B)
+    _, rep, _ = solve_block_gmres(A, B, None, SolverConfig(m=6, tol=1e-10, max_cycles=30))
+    _compare_report(rep, g, "small/gmres/", bnorm)
+    _, rep, rs = solve_block_gcrodr(A, B, None, SolverConfig(m=6, k=4, tol=1e-10, max_cycles=30))
+    _compare_report(rep, g, "small/gcrodr/", bnorm)
+    _, rep, _ = solve_block_gcrodr(A, B[:, :1], None, SolverConfig(m=6, k=4, block_width=3, tol=1e-10,
+                                                                  max_cycles=30))
+    _compare_report(rep, g, "small/enlarged/", bnorm)
+    _, rep, _ = solve_block_gcrodr(A, B, None, SolverConfig(m=6, k=4, tol=1e-10, max_cycles=30,
+                                                           stop_rule="per-column-relative", early_exit=False))
+    _compare_report(rep, g, "small/percol/", bnorm)
+
+
+def test_recycling_golden(cuda):
+    from paper_1604_01713_b200.recycling import (RecycleSpace, harmonic_ritz_augmented, harmonic_ritz_krylov,
+                                                 prepare_cross_system, update_recycle_space)
+    from paper_1604_01713_b200.solver import _Operator
+
+    g = load_golden("recycling_cases.npz")
+    A = csr_matrix_from(g, "A/")
+    W, H = g["kry/W"], g["kry/H"]
+    L = 2
+    m = H.shape[1] // L
+    fact = _fact_from(W, H, np.zeros((0, 0)), m, L, 0, cuda)
+    sel = harmonic_ritz_krylov(fact, k_target=5)
+    assert np.allclose(sel.pairs.values, g["kry/values"], rtol=1e-10, atol=1e-12)
+    assert sel.keep.tolist() == g["kry/keep"].tolist()
+    rs1 = update_recycle_space(fact, None, sel, 5)
+    U1, C1 = rs1.numpy()
+    assert np.abs(U1 - g["kry/U"]).max() <= 1e-10 * np.abs(g["kry/U"]).max()
+    assert np.abs(C1 - g["kry/C"]).max() <= 1e-10
+    # augmented problem on the golden factorization
+    rs_in = RecycleSpace(u=g["kry/U"], c=g["kry/C"])
+    W2, H2, F2 = g["aug/W"], g["aug/H"], g["aug/F"]
+    m2 = H2.shape[1] // L
+    fact2 = _fact_from(W2, H2, F2, m2, L, rs_in.k, cuda)
+    sel2 = harmonic_ritz_augmented(fact2, rs_in, g["aug/d"], k_target=5)
+    assert np.allclose(sel2.pairs.values, g["aug/values"], rtol=1e-8, atol=1e-10)
+    assert sel2.keep.tolist() == g["aug/keep"].tolist()
+    rs2 = update_recycle_space(fact2, rs_in, sel2, 5)
+    U2, C2 = rs2.numpy()
+    # eigenvectors are defined up to scale/sign: compare the spanned spaces
+    assert np.linalg.norm(C2 @ C2.T - g["aug/C"] @ g["aug/C"].T) <= 1e-8
+    # cross-system preparation
+    A2 = csr_matrix_from(g, "A2/")
+    rs3 = prepare_cross_system(RecycleSpace(u=g["aug/U"], c=g["aug/C"]), _Operator(A2, None, "none").apply)
+    U3, C3 = rs3.numpy()
+    assert np.abs(C3 - g["cross/C"]).max() <= 1e-10
+    assert np.abs(U3 - g["cross/U"]).max() <= 1e-9 * np.abs(g["cross/U"]).max()

@@ -1,0 +1,57 @@
+"""Pin the oracle (oracle/) to golden vectors produced by the real
+reference (tests/golden/make_golden.py) — CPU only."""
+
+import numpy as np
+
+import oracle
+from conftest import csr_from, load_golden
+
+
+def test_oracle_spmm_bitwise_vs_reference():
+    g = load_golden("spmm_cases.npz")
+    for name in g["cases"]:
+        rp, ci, v, shape = csr_from(g, f"{name}/")
+        for threads in (1, 3):
+            Y = oracle.spmm(rp, ci, v, g[f"{name}/X"], nthreads=threads)
+            assert np.array_equal(Y, g[f"{name}/Y"]), name
+
+
+def test_oracle_reduced_qr_vs_reference():
+    g = load_golden("qr_cases.npz")
+    for name in g["cases"]:
+        q, r, flagged = oracle.reduced_qr(g[f"{name}/X"])
+        assert flagged.tolist() == g[f"{name}/flagged"].tolist(), name
+        # same LAPACK, same sign fix: identical up to threading noise
+        assert np.abs(r - g[f"{name}/r"]).max() <= 1e-13 * max(np.abs(r).max(), 1.0), name
+        ok = ~flagged
+        assert np.abs(q[:, ok] - g[f"{name}/q"][:, ok]).max() <= 1e-12, name
+
+
+def test_oracle_arnoldi_step_vs_reference():
+    """Replay each golden step: V_j, the basis V_1..V_j and C must give the
+    golden H / F columns and V_{j+1} (arnoldi.py:139-193)."""
+    g = load_golden("arnoldi_cases.npz")
+    for name in g["cases"]:
+        rp, ci, v, shape = csr_from(g, f"{name}/")
+        W, H, F = g[f"{name}/W"], g[f"{name}/H"], g[f"{name}/F"]
+        m, k = int(g[f"{name}/m"]), int(g[f"{name}/k"])
+        L = W.shape[1] // (m + 1)
+        C = g[f"{name}/C"] if k else None
+        scale = np.abs(v).sum()
+        for j in range(m):
+            Vm = W[:, j * L:(j + 1) * L]
+            q, Fc, Hc, r, flagged = oracle.arnoldi_step(rp, ci, v, Vm, C, W[:, :(j + 1) * L])
+            cols = slice(j * L, (j + 1) * L)
+            assert np.abs(Hc - H[:(j + 1) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            assert np.abs(r - H[(j + 1) * L:(j + 2) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            if k:
+                assert np.abs(Fc - F[:, cols]).max() <= 1e-12 * scale, (name, j)
+            if not flagged.any():
+                assert np.abs(q - W[:, (j + 1) * L:(j + 2) * L]).max() <= 1e-10, (name, j)
+
+
+def test_oracle_bytes_model_vs_reference():
+    g = load_golden("bench_model.npz")
+    assert oracle.spmm_bytes(5, 7, 3) == int(g["matvec_bytes_5_7_3"])
+    for p, ref in zip((1, 2, 4, 8, 16), g["matvec_bytes_cfg2"]):
+        assert oracle.spmm_bytes(2097152, 14581760, p) == int(ref)
