@@ -54,9 +54,24 @@ spmm_csr_kernel(int64_t row_begin, int64_t row_end,
   double* sva = s_va[w];
   for (int32_t base = wbeg; base < wend; base += kSpmmChunk) {
     const int32_t cnt = min(kSpmmChunk, wend - base);
-    for (int e = lane; e < cnt; e += 32) {
-      sci[e] = __ldg(ci + base + e);
-      sva[e] = __ldg(va + base + e);
+    // all loads of the chunk are issued before the first shared-memory store
+    int32_t ci_r[kSpmmChunk / 32];
+    double va_r[kSpmmChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kSpmmChunk / 32; ++u) {
+      const int e = lane + 32 * u;
+      if (e < cnt) {
+        ci_r[u] = __ldg(ci + base + e);
+        va_r[u] = __ldg(va + base + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSpmmChunk / 32; ++u) {
+      const int e = lane + 32 * u;
+      if (e < cnt) {
+        sci[e] = ci_r[u];
+        sva[e] = va_r[u];
+      }
     }
     __syncwarp();
     const int lo = max(mybeg, base) - base;

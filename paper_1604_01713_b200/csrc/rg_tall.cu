@@ -31,6 +31,9 @@
 // the FP64 tensor path on sm_100a.
 #include "rg_common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace rg {
 
 constexpr int kTallThreads = 256;  // = tile rows R
@@ -300,6 +303,219 @@ __global__ void __launch_bounds__(kTallThreads, 1) tall_kernel(TallParams P) {
   if (threadIdx.x == 0) *P.counter = 0u;  // re-arm for the next launch on this workspace
 }
 
+
+// ============================================================================
+// Warp-autonomous streaming kernel (the production path).
+//
+// Measured on B200 (tools/microbench.cu -> profiles/microbench_r01.txt):
+// lane-per-row LDG streams column-major blocks at 6.9-7.3 TB/s; FP64 DMMA
+// m8n8k4 sustains ~37 TFLOP/s; 1-D bulk copies are request-rate bound (one
+// request per ~60 cycles per SM: 512-byte column copies cap at 2.4 TB/s);
+// DMMA fragments loaded straight from HBM touch 8 lines per instruction and
+// make the kernel L1-wavefront bound.  Hence:
+//
+//   every warp owns 32 consecutive rows at a time (no CTA barrier inside the
+//   loop; lane = row, so every load instruction is one 256-byte segment):
+//   phase 1  z = Zin + sum_t alpha_t X_t S_t with DFMA (S rows read as smem
+//            broadcasts), z = z R1^-1 R2^-1 row-wise, Zout store, norms
+//   phase 2  Gram += Gb^T z on DMMA: the Gb block is loaded lane-per-row in
+//            8-column slabs (next slab prefetched into registers), staged
+//            through a warp-private padded smem slab, and read back as
+//            conflict-free m8n8k4 fragments; z comes from a warp tile.
+//   epilogue warp partials summed in warp order, CTA partial to the
+//            workspace, the last CTA sums the partials in CTA order.
+// ============================================================================
+
+constexpr int kV3Warps = 8;
+constexpr int kV3Threads = kV3Warps * 32;
+constexpr int kSlabStride = 36;  // 32 rows + 4: conflict-free fragment reads
+
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kV3Threads, 2) tall_v3_kernel(TallParams P) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  extern __shared__ __align__(16) double smem[];
+  const int p = P.p;
+  double* sS1 = smem;                          // [a1][PM] row-major
+  double* sS2 = sS1 + P.a1 * PM;               // [a2][PM]
+  double* sR1 = sS2 + P.a2 * PM;               // PM x PM row-major
+  double* sR2 = sR1 + PM * PM;
+  double* wbase = sR2 + PM * PM;               // per warp: z tile [PM8][36] + 2 slabs [8][36]
+  constexpr int kWarpWords = PM8 * kSlabStride + 2 * 8 * kSlabStride;
+  double* red = wbase + kV3Warps * kWarpWords; // epilogue
+
+  for (int e = threadIdx.x; e < P.a1 * PM; e += kV3Threads) {
+    const int aa = e / PM, c = e % PM;
+    sS1[e] = c < p ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
+  }
+  for (int e = threadIdx.x; e < P.a2 * PM; e += kV3Threads) {
+    const int aa = e / PM, c = e % PM;
+    sS2[e] = c < p ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
+  }
+  for (int e = threadIdx.x; e < PM * PM; e += kV3Threads) {
+    const int ii = e / PM, jj = e % PM;
+    const double id = ii == jj ? 1.0 : 0.0;
+    sR1[e] = (P.r1 && ii < p && jj < p) ? P.r1[ii + (int64_t)jj * p] : id;
+    sR2[e] = (P.r2 && ii < p && jj < p) ? P.r2[ii + (int64_t)jj * p] : id;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  double* zt = wbase + warp * kWarpWords;       // [PM8][36]
+  double* slab = zt + PM8 * kSlabStride;        // [2][8][36]
+  const bool gram_tile = (P.gmode == 1 || P.gmode == 2);
+  const int mtiles = P.mtiles;
+
+  double acc[MTMAX][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MTMAX; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  const int64_t nunits = (P.n + 31) / 32;
+  const int64_t gwarp = (int64_t)blockIdx.x * kV3Warps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kV3Warps;
+  for (int64_t u = gwarp; u < nunits; u += nwarps) {
+    const int64_t r0 = u * 32;
+    const int64_t i = r0 + lane;
+    const bool valid = i < P.n;
+    // ---------------- phase 1: lane = row
+    double z[PM];
+#pragma unroll
+    for (int c = 0; c < PM; ++c) z[c] = 0.0;
+    if (valid) {
+      if (P.zin) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) z[c] = __ldg(P.zin + i + (int64_t)c * P.ldzin);
+      }
+      if (P.a1) apply_term<PM>(z, P.x1, P.ldx1, P.a1, sS1, P.alpha1, i);
+      if (P.a2) apply_term<PM>(z, P.x2, P.ldx2, P.a2, sS2, P.alpha2, i);
+      if (P.r1) trsm_row<PM>(z, sR1, p);
+      if (P.r2) trsm_row<PM>(z, sR2, p);
+      if (P.zout) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) P.zout[i + (int64_t)c * P.ldzout] = z[c];
+      }
+      if (P.gmode == 3) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) sq[c] = fma(z[c], z[c], sq[c]);
+      }
+    }
+    if (!gram_tile) continue;
+    // ---------------- phase 2: DMMA Gram over these 32 rows (8 k-steps)
+#pragma unroll
+    for (int c = 0; c < PM8; ++c) zt[c * kSlabStride + lane] = c < PM ? z[c < PM ? c : 0] : 0.0;
+    __syncwarp();
+    if (P.gmode == 2) {
+#pragma unroll
+      for (int mt = 0; mt < MTMAX; ++mt) {
+        if (mt < mtiles) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = zt[(mt * 8 + mrow) * kSlabStride + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSlabStride + ks * 4 + kq]);
+          }
+        }
+      }
+    } else {
+      double g[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        g[c] = (valid && c < P.gc) ? __ldg(P.gb + i + (int64_t)c * P.ldgb) : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MTMAX; ++mt) {
+        if (mt < mtiles) {
+          double* sl = slab + (mt & 1) * 8 * kSlabStride;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) sl[c * kSlabStride + lane] = g[c];
+          if (mt + 1 < mtiles) {  // prefetch the next 8-column slab
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int gg = (mt + 1) * 8 + c;
+              g[c] = (valid && gg < P.gc) ? __ldg(P.gb + i + (int64_t)gg * P.ldgb) : 0.0;
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = sl[mrow * kSlabStride + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSlabStride + ks * 4 + kq]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  // ---------------- epilogue: deterministic reductions
+  __shared__ bool s_last;
+  __syncthreads();
+  if (gram_tile) {
+    for (int ww = 0; ww < kV3Warps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTMAX; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+                red[idx] = (ww == 0) ? acc[mt][nt][v] : red[idx] + acc[mt][nt][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kV3Threads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = red[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kV3Threads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kV3Warps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = (P.gmode == 3) ? p : P.gc * p;
+  for (int e = threadIdx.x; e < ne; e += kV3Threads) {
+    double sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = sum;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
 static int pick_pm(int p) {
   if (p <= 1) return 1;
   if (p <= 2) return 2;
@@ -341,6 +557,42 @@ static cudaError_t launch_tall(const TallParams& P, size_t smem, int64_t max_gri
   k<<<(unsigned)g, kTallThreads, smem, st>>>(P);
   return cudaGetLastError();
 }
+
+
+template <int PM, int MTMAX>
+static cudaError_t launch_v3(const TallParams& P, int64_t max_grid, cudaStream_t st) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  auto k = tall_v3_kernel<PM, MTMAX>;
+  constexpr int kWarpWords = PM8 * kSlabStride + 2 * 8 * kSlabStride;
+  const size_t smem = ((size_t)(P.a1 + P.a2) * PM + 2 * PM * PM + (size_t)kV3Warps * kWarpWords +
+                       (size_t)std::max(MTMAX * NT * 64, kV3Warps * PM)) * sizeof(double);
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kV3Threads, 64 * 1024);
+    per_sm = v < 1 ? 1 : v;
+  }
+  const int64_t nunits = (P.n + 31) / 32;
+  int64_t g = (int64_t)sm_count() * per_sm;
+  if (g > max_grid) g = max_grid;
+  const int64_t need = (nunits + kV3Warps - 1) / kV3Warps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kV3Threads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+#define RG_V3_CASE(PMv)                                                                   \
+  case PMv:                                                                               \
+    switch (mtmax) {                                                                      \
+      case 2: e = launch_v3<PMv, 2>(P, bound, st); break;                                 \
+      case 6: e = launch_v3<PMv, 6>(P, bound, st); break;                                 \
+      case 12: e = launch_v3<PMv, 12>(P, bound, st); break;                               \
+      default: e = launch_v3<PMv, 16>(P, bound, st); break;                               \
+    }                                                                                     \
+    break;
 
 // upper bound on the grid of any rg_tall launch (workspace sizing)
 static int64_t tall_grid_bound() { return (int64_t)sm_count() * 2; }
@@ -413,6 +665,20 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const int64_t bound = tall_grid_bound();
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
+  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512) {
+    switch (PM) {
+      RG_V3_CASE(1)
+      RG_V3_CASE(2)
+      RG_V3_CASE(4)
+      RG_V3_CASE(8)
+      RG_V3_CASE(16)
+    }
+    if (e != cudaSuccess) {
+      set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+      return RG_ECUDA;
+    }
+    return RG_OK;
+  }
   switch (PM) {
     RG_TALL_CASE(1)
     RG_TALL_CASE(2)

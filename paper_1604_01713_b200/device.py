@@ -321,8 +321,17 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
             gmode, gout = 3, gram[1]
         else:
             raise ValueError(f"unknown gram kind {kind!r}")
-    # passes over the term list (<= 2 terms each)
-    groups = [terms[i:i + 2] for i in range(0, len(terms), 2)] or [[]]
+    # passes over the term list (<= 2 terms and <= MAX_TERM_COLS staged columns each)
+    groups, cur_g, cur_cols = [], [], 0
+    for t in terms:
+        a = t[0].shape[1]
+        if cur_g and (len(cur_g) == 2 or cur_cols + a > MAX_TERM_COLS):
+            groups.append(cur_g)
+            cur_g, cur_cols = [], 0
+        cur_g.append(t)
+        cur_cols += a
+    if cur_g or not groups:
+        groups.append(cur_g)
     needs_multi = len(groups) > 1 or (gmode == 1 and gb.shape[1] > MAX_GC)
     zbuf = Z_out
     if needs_multi and zbuf is None:

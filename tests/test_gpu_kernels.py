@@ -198,15 +198,20 @@ def test_reduced_qr_golden(cuda):
         flagged = g[f"{name}/flagged"]
         assert f.flagged.tolist() == flagged.tolist(), name
         assert f.rank == int(g[f"{name}/rank"]), name
-        cond = np.linalg.cond(X) if not flagged.any() else 1.0
-        ok = ~flagged
+        # columns from the first flagged one on are determined by rounding
+        # noise in any QR (the direction LAPACK picks for a dependent column
+        # is arbitrary); compare the leading well-determined block exactly
+        # and the factorisation properties everywhere
+        j0 = int(np.argmax(flagged)) if flagged.any() else X.shape[1]
+        lead = X[:, :j0]
+        cond = np.linalg.cond(lead) if j0 else 1.0
         tol = 1e-12 * max(cond, 1.0) * max(np.abs(r_ref).max(), 1.0)
-        # R rows of flagged columns are rounding noise in both implementations
-        assert np.abs(f.r_factor[np.ix_(ok, ok)] - r_ref[np.ix_(ok, ok)]).max() <= tol, name
+        assert np.abs(f.r_factor[:j0, :] - r_ref[:j0, :]).max(initial=0.0) <= tol, name
         assert np.all(np.diagonal(f.r_factor) >= 0.0)
         q = f.q
-        assert np.abs(q[:, ok] - g[f"{name}/q"][:, ok]).max() <= 1e-12 * max(cond, 1.0) * 10, name
+        assert np.abs(q[:, :j0] - g[f"{name}/q"][:, :j0]).max(initial=0.0) <= 1e-11 * max(cond, 1.0), name
         assert np.linalg.norm(q.T @ q - np.eye(q.shape[1])) <= 1e-12 * q.shape[1]
+        assert np.linalg.norm(q @ f.r_factor - X) <= 1e-13 * max(np.linalg.norm(X), 1e-300) * X.shape[1]
 
 
 def test_reduced_qr_rejects_wide(cuda):
