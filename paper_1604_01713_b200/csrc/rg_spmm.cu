@@ -24,14 +24,14 @@ namespace rg {
 constexpr int kSpmmWarps = 8;     // 256 threads per CTA
 constexpr int kSpmmChunk = 256;   // staged nonzeros per warp per round
 
-template <int PB>
+template <int PB, bool GHOST>
 __global__ void __launch_bounds__(kSpmmWarps * 32)
 spmm_csr_kernel(int64_t row_begin, int64_t row_end,
                 const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                 const double* __restrict__ va,
                 const double* __restrict__ X, int64_t ldx, int64_t n_local,
                 const double* __restrict__ Xg, int64_t ldg,
-                int pc, double* __restrict__ Y, int64_t ldy) {
+                double* __restrict__ Y, int64_t ldy) {
   __shared__ int32_t s_ci[kSpmmWarps][kSpmmChunk];
   __shared__ double s_va[kSpmmWarps][kSpmmChunk];
   const int lane = threadIdx.x & 31;
@@ -76,43 +76,58 @@ spmm_csr_kernel(int64_t row_begin, int64_t row_end,
     __syncwarp();
     const int lo = max(mybeg, base) - base;
     const int hi = min(myend, base + cnt) - base;
-#pragma unroll 4
-    for (int t = lo; t < hi; ++t) {
-      const double a = sva[t];
+    // software pipeline: the PB gathers of nonzero t+1 are in flight while
+    // nonzero t is accumulated (in the reference's order: t ascending)
+    double xn[PB];
+    double an = 0.0;
+    auto gather = [&](int t, double (&xv)[PB]) {
       const int64_t j = sci[t];
-      const double* xp;
-      int64_t ld;
-      if (j < n_local) {
-        xp = X + j;
-        ld = ldx;
-      } else {
+      const double* xp = X + j;
+      int64_t ld = ldx;
+      if (GHOST && j >= n_local) {
         xp = Xg + (j - n_local);
         ld = ldg;
       }
 #pragma unroll
-      for (int c = 0; c < PB; ++c) {
-        if (PB == 1 || c < pc) acc[c] = __dadd_rn(acc[c], __dmul_rn(a, __ldg(xp + c * ld)));
+      for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
+    };
+    if (lo < hi) {
+      an = sva[lo];
+      gather(lo, xn);
+    }
+    for (int t = lo; t < hi; ++t) {
+      double xc[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) xc[c] = xn[c];
+      const double ac = an;
+      if (t + 1 < hi) {
+        an = sva[t + 1];
+        gather(t + 1, xn);
       }
+#pragma unroll
+      for (int c = 0; c < PB; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(ac, xc[c]));
     }
     __syncwarp();
   }
   if (valid) {
 #pragma unroll
-    for (int c = 0; c < PB; ++c)
-      if (PB == 1 || c < pc) Y[i + c * ldy] = acc[c];
+    for (int c = 0; c < PB; ++c) Y[i + c * ldy] = acc[c];
   }
 }
 
 template <int PB>
 static void launch_spmm(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci,
                         const double* va, const double* X, int64_t ldx, int64_t n_local,
-                        const double* Xg, int64_t ldg, int pc, double* Y, int64_t ldy,
-                        cudaStream_t s) {
+                        const double* Xg, int64_t ldg, double* Y, int64_t ldy, cudaStream_t s) {
   const int64_t rows = re - rb;
   const int64_t rows_per_cta = kSpmmWarps * 32;
   const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
-  spmm_csr_kernel<PB><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(
-      rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg, pc, Y, ldy);
+  if (Xg)
+    spmm_csr_kernel<PB, true><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                        Xg, ldg, Y, ldy);
+  else
+    spmm_csr_kernel<PB, false><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                         Xg, ldg, Y, ldy);
 }
 
 }  // namespace rg
@@ -135,22 +150,27 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
              "rg_spmm_csr_f64: ldx=%lld < n_local=%lld", (long long)ldx, (long long)n_local);
   if (row_end == row_begin) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  for (int c0 = 0; c0 < p; c0 += 16) {
-    const int pc = p - c0 < 16 ? p - c0 : 16;
+  // exact-width passes (no per-column predication in the inner loop):
+  // 16-wide passes, then one pass of the remaining width
+  for (int c0 = 0; c0 < p;) {
+    const int rem = p - c0;
+    const int pc = rem >= 16 ? 16 : (rem > 8 ? 8 : rem);
     const double* X = d_x ? d_x + (int64_t)c0 * ldx : nullptr;
     const double* Xg = d_xg ? d_xg + (int64_t)c0 * ldg : nullptr;
     double* Y = d_y + (int64_t)c0 * ldy;
-    if (pc == 1)
-      launch_spmm<1>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, pc, Y, ldy, s);
-    else if (pc == 2)
-      launch_spmm<2>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, pc, Y, ldy, s);
-    else if (pc <= 4)
-      launch_spmm<4>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, pc, Y, ldy, s);
-    else if (pc <= 8)
-      launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, pc, Y, ldy, s);
-    else
-      launch_spmm<16>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, pc, Y, ldy, s);
+    switch (pc) {
+      case 1: launch_spmm<1>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 2: launch_spmm<2>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 3: launch_spmm<3>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 4: launch_spmm<4>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 5: launch_spmm<5>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 6: launch_spmm<6>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 7: launch_spmm<7>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 8: launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      default: launch_spmm<16>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+    }
     RG_CHECK_LAUNCH("rg_spmm_csr_f64");
+    c0 += pc;
   }
   return RG_OK;
 }

@@ -109,14 +109,15 @@ __device__ __forceinline__ void apply_term(double (&z)[PM], const double* __rest
 
 template <int PM>
 __device__ __forceinline__ void trsm_row(double (&z)[PM], const double* sR, int p) {
-  // y R = z with R upper triangular (row-major [i*PM + j] in smem)
+  // y R = z with R upper triangular (row-major [i*PM + j] in smem, diagonal
+  // stored as reciprocals so the dependent chain has no divisions)
 #pragma unroll
   for (int j = 0; j < PM; ++j) {
     if (j < p) {
       double y = z[j];
 #pragma unroll
       for (int k = 0; k < j; ++k) y = fma(-z[k], sR[k * PM + j], y);
-      z[j] = y / sR[j * PM + j];
+      z[j] = y * sR[j * PM + j];  // the diagonal slot holds 1 / r_jj
     }
   }
 }
@@ -145,12 +146,12 @@ __global__ void __launch_bounds__(kTallThreads, 1) tall_kernel(TallParams P) {
   if (P.r1)
     for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
       const int ii = e / PM, jj = e % PM;
-      sR1[e] = (ii < p && jj < p) ? P.r1[ii + (int64_t)jj * p] : (ii == jj ? 1.0 : 0.0);
+      sR1[e] = (ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : (ii == jj ? 1.0 : 0.0);
     }
   if (P.r2)
     for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
       const int ii = e / PM, jj = e % PM;
-      sR2[e] = (ii < p && jj < p) ? P.r2[ii + (int64_t)jj * p] : (ii == jj ? 1.0 : 0.0);
+      sR2[e] = (ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : (ii == jj ? 1.0 : 0.0);
     }
   __syncthreads();
 
@@ -355,8 +356,8 @@ __global__ void __launch_bounds__(kV3Threads, 2) tall_v3_kernel(TallParams P) {
   for (int e = threadIdx.x; e < PM * PM; e += kV3Threads) {
     const int ii = e / PM, jj = e % PM;
     const double id = ii == jj ? 1.0 : 0.0;
-    sR1[e] = (P.r1 && ii < p && jj < p) ? P.r1[ii + (int64_t)jj * p] : id;
-    sR2[e] = (P.r2 && ii < p && jj < p) ? P.r2[ii + (int64_t)jj * p] : id;
+    sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
+    sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
   }
   __syncthreads();
 
@@ -516,6 +517,279 @@ __global__ void __launch_bounds__(kV3Threads, 2) tall_v3_kernel(TallParams P) {
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
+// ============================================================================
+// v5: v3's lane-per-row update + a cp.async ring for the Gram basis slabs.
+//
+// ncu on v3 (profiles/): 61% long-scoreboard stalls -- each unit exposed
+// ~13 dependent load rounds (update batches, then one-slab-ahead Gram
+// prefetch).  A full cp.async ring for every operand (v4) hid the latency
+// but doubled the instruction count (issue bound).  Here only the Gram basis
+// goes through the ring, with compile-time slots: a unit's first kRing5
+// slabs are issued before its update phase (they do not depend on z), land
+// while the DFMA update runs, and DMMA fragments are read straight from the
+// landed slab (no staging stores).  The update's column batches are
+// software-pipelined (batch b+1 in flight while batch b is accumulated).
+// ============================================================================
+
+constexpr int kV5Warps = 8;
+constexpr int kV5Threads = kV5Warps * 32;
+constexpr int kRing5 = 4;
+constexpr int kSS5 = 36;
+
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// 8 columns x 32 rows of Gb into a slab: 4 chunks of 16 B per lane
+__device__ __forceinline__ void gb_slab(double* slot, const double* gb, int64_t ldgb, int gc, int col0,
+                                        int64_t r0, int64_t n, int lane) {
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int e = lane + 32 * t;
+    const int c = e >> 4, rp = e & 15;
+    const int64_t row = r0 + 2 * rp;
+    int64_t vr = n - row;
+    vr = vr < 0 ? 0 : (vr > 2 ? 2 : vr);
+    const int bytes = (col0 + c < gc) ? (int)vr * 8 : 0;
+    const double* src = bytes ? gb + row + (int64_t)(col0 + c) * ldgb : gb;
+    cp_async16(slot + c * kSS5 + 2 * rp, src, bytes);
+  }
+}
+
+template <int PM>
+__device__ __forceinline__ void apply_term_pipe(double (&z)[PM], const double* __restrict__ X, int64_t ldx,
+                                                int a, const double* sS, double alpha, int64_t i) {
+  // batches of 8 columns; batch b+1 is loaded while batch b is accumulated
+  double m[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) m[c] = 0.0;
+  double xn[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) xn[u] = u < a ? __ldg(X + i + (int64_t)u * ldx) : 0.0;
+  for (int a0 = 0; a0 < a; a0 += 8) {
+    double xc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xc[u] = xn[u];
+    if (a0 + 8 < a) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xn[u] = a0 + 8 + u < a ? __ldg(X + i + (int64_t)(a0 + 8 + u) * ldx) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (a0 + u < a) {
+        const double* srow = sS + (a0 + u) * PM;
+#pragma unroll
+        for (int c = 0; c < PM; ++c) m[c] = fma(xc[u], srow[c], m[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < PM; ++c) z[c] = z[c] + alpha * m[c];
+}
+
+template <int MTMAX>
+struct V5MinBlocks {
+  static constexpr int value = 2;
+};
+
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kV5Threads, V5MinBlocks<MTMAX>::value) tall_v5_kernel(TallParams P) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  constexpr int kWarpWords = kRing5 * 8 * kSS5 + PM8 * kSS5;
+  extern __shared__ __align__(16) double smem[];
+  const int p = P.p;
+  double* sS1 = smem;                          // [a1][PM] row-major
+  double* sS2 = sS1 + P.a1 * PM;               // [a2][PM]
+  double* sR1 = sS2 + P.a2 * PM;               // PM x PM row-major
+  double* sR2 = sR1 + PM * PM;
+  double* wbase = sR2 + PM * PM;
+  wbase += ((uintptr_t)wbase & 15) ? 1 : 0;    // 16-byte alignment for cp.async
+  double* red = wbase + kV5Warps * kWarpWords;
+
+  for (int e = threadIdx.x; e < P.a1 * PM; e += kV5Threads) {
+    const int aa = e / PM, c = e % PM;
+    sS1[e] = c < p ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
+  }
+  for (int e = threadIdx.x; e < P.a2 * PM; e += kV5Threads) {
+    const int aa = e / PM, c = e % PM;
+    sS2[e] = c < p ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
+  }
+  for (int e = threadIdx.x; e < PM * PM; e += kV5Threads) {
+    const int ii = e / PM, jj = e % PM;
+    const double id = ii == jj ? 1.0 : 0.0;
+    sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
+    sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  double* ring = wbase + warp * kWarpWords;     // [kRing5][8][kSS5]
+  double* zt = ring + kRing5 * 8 * kSS5;        // [PM8][kSS5]
+  const bool gram_tile = MTMAX > 0 && (P.gmode == 1 || P.gmode == 2);
+  const int mtiles = P.mtiles;
+  const bool basis = P.gmode == 1;
+  constexpr int MTA = MTMAX > 0 ? MTMAX : 1;
+
+  double acc[MTA][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MTA; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  const int64_t nunits = (P.n + 31) / 32;
+  const int64_t gwarp = (int64_t)blockIdx.x * kV5Warps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kV5Warps;
+  for (int64_t u = gwarp; u < nunits; u += nwarps) {
+    const int64_t r0 = u * 32;
+    const int64_t i = r0 + lane;
+    const bool valid = i < P.n;
+    // Gram slabs 0..kRing5-1 start landing now (independent of z)
+    if (basis) {
+#pragma unroll
+      for (int s = 0; s < kRing5; ++s) {
+        if (s < mtiles) gb_slab(ring + s * 8 * kSS5, P.gb, P.ldgb, P.gc, s * 8, r0, P.n, lane);
+        cp_async_commit();
+      }
+    }
+    // ---------------- phase 1: lane = row
+    double z[PM];
+#pragma unroll
+    for (int c = 0; c < PM; ++c) z[c] = 0.0;
+    if (valid) {
+      if (P.zin) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) z[c] = __ldg(P.zin + i + (int64_t)c * P.ldzin);
+      }
+      if (P.a1) apply_term_pipe<PM>(z, P.x1, P.ldx1, P.a1, sS1, P.alpha1, i);
+      if (P.a2) apply_term_pipe<PM>(z, P.x2, P.ldx2, P.a2, sS2, P.alpha2, i);
+      if (P.r1) trsm_row<PM>(z, sR1, p);
+      if (P.r2) trsm_row<PM>(z, sR2, p);
+      if (P.zout) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) P.zout[i + (int64_t)c * P.ldzout] = z[c];
+      }
+      if (P.gmode == 3) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) sq[c] = fma(z[c], z[c], sq[c]);
+      }
+    }
+    if (!gram_tile) continue;
+    // ---------------- phase 2: DMMA Gram over these 32 rows (8 k-steps)
+#pragma unroll
+    for (int c = 0; c < PM8; ++c) zt[c * kSS5 + lane] = c < PM ? z[c < PM ? c : 0] : 0.0;
+    __syncwarp();
+    if (!basis) {
+#pragma unroll
+      for (int mt = 0; mt < MTMAX; ++mt) {
+        if (mt < mtiles) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = zt[(mt * 8 + mrow) * kSS5 + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSS5 + ks * 4 + kq]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MTMAX; ++mt) {
+        if (mt < mtiles) {
+          cp_async_wait<kRing5 - 1>();
+          __syncwarp();
+          const double* sl = ring + (mt % kRing5) * 8 * kSS5;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = sl[mrow * kSS5 + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSS5 + ks * 4 + kq]);
+          }
+          __syncwarp();
+          if (mt + kRing5 < mtiles)
+            gb_slab(ring + (mt % kRing5) * 8 * kSS5, P.gb, P.ldgb, P.gc, (mt + kRing5) * 8, r0, P.n, lane);
+          cp_async_commit();
+        }
+      }
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+  }
+
+  // ---------------- epilogue: deterministic reductions
+  __shared__ bool s_last;
+  __syncthreads();
+  if (gram_tile) {
+    for (int ww = 0; ww < kV5Warps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTMAX; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+                red[idx] = (ww == 0) ? acc[mt][nt][v] : red[idx] + acc[mt][nt][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kV5Threads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = red[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kV5Threads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kV5Warps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = (P.gmode == 3) ? p : P.gc * p;
+  for (int e = threadIdx.x; e < ne; e += kV5Threads) {
+    double sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = sum;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
 static int pick_pm(int p) {
   if (p <= 1) return 1;
   if (p <= 2) return 2;
@@ -594,6 +868,46 @@ static cudaError_t launch_v3(const TallParams& P, int64_t max_grid, cudaStream_t
     }                                                                                     \
     break;
 
+template <int PM, int MTMAX>
+static cudaError_t launch_v5(const TallParams& P, int64_t max_grid, cudaStream_t st) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  constexpr int kWarpWords = kRing5 * 8 * kSS5 + PM8 * kSS5;
+  auto k = tall_v5_kernel<PM, MTMAX>;
+  const size_t smem = ((size_t)(P.a1 + P.a2) * PM + 2 * PM * PM + 2 + (size_t)kV5Warps * kWarpWords +
+                       (size_t)std::max(MTMAX * NT * 64, kV5Warps * PM)) * sizeof(double);
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kV5Threads, smem);
+    per_sm = v < 1 ? 1 : v;
+  }
+  const int64_t nunits = (P.n + 31) / 32;
+  int64_t g = (int64_t)sm_count() * per_sm;
+  if (g > max_grid) g = max_grid;
+  const int64_t need = (nunits + kV5Warps - 1) / kV5Warps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kV5Threads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+#define RG_V5_CASE(PMv)                                                                   \
+  case PMv:                                                                               \
+    switch (mt5) {                                                                      \
+      case 0: e = launch_v5<PMv, 0>(P, bound, st); break;                                 \
+      case 2: e = launch_v5<PMv, 2>(P, bound, st); break;                                 \
+      case 6: e = launch_v5<PMv, 6>(P, bound, st); break;                                 \
+      case 12: e = launch_v5<PMv, 12>(P, bound, st); break;                               \
+      default: e = launch_v5<PMv, 16>(P, bound, st); break;                               \
+    }                                                                                     \
+    break;
+
+static bool aligned16(const void* p, int64_t ld) {
+  return p == nullptr || (((uintptr_t)p & 15u) == 0 && (ld & 1) == 0);
+}
+
 // upper bound on the grid of any rg_tall launch (workspace sizing)
 static int64_t tall_grid_bound() { return (int64_t)sm_count() * 2; }
 
@@ -665,13 +979,28 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const int64_t bound = tall_grid_bound();
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512) {
+  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512 && aligned16(P.zin, P.ldzin) &&
+      aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) && (gram_mode != 1 || aligned16(P.gb, P.ldgb)) ) {
+    const char* impl = getenv("RG_TALL_IMPL");
+    const int mt5 = (gram_mode == 1 || gram_mode == 2) ? mtmax : 0;
+    // v5 (cp.async Gram ring) wins for basis Grams, v3 for the rest
+    // (tools/ab_tall.sh, profiles/ab_tall_r01.txt)
+    const bool use_v5 = impl ? impl[0] == '5' : gram_mode == 1;
+    if (!use_v5) {
+      switch (PM) {
+        RG_V3_CASE(1)
+        RG_V3_CASE(2)
+        RG_V3_CASE(4)
+        RG_V3_CASE(8)
+        RG_V3_CASE(16)
+      }
+    } else
     switch (PM) {
-      RG_V3_CASE(1)
-      RG_V3_CASE(2)
-      RG_V3_CASE(4)
-      RG_V3_CASE(8)
-      RG_V3_CASE(16)
+      RG_V5_CASE(1)
+      RG_V5_CASE(2)
+      RG_V5_CASE(4)
+      RG_V5_CASE(8)
+      RG_V5_CASE(16)
     }
     if (e != cudaSuccess) {
       set_error("rg_tall_f64: %s", cudaGetErrorString(e));
