@@ -119,8 +119,13 @@ class ArnoldiFactorization:
         reference), CGS twice against ``bases`` on the device.  Returns
         (vector, norm) or (None, 0)."""
         scratch = [torch.zeros(b.shape[1], dtype=torch.float64, device=self.device).view(-1, 1) for b in bases]
+        part = _dev.get_part()
         for _ in range(tries):
-            v = _dev.to_device_block(self._rng.standard_normal(self.n).reshape(-1, 1))
+            if part is None:
+                draw = self._rng.standard_normal(self.n)
+            else:  # same global stream as one process, sliced to this rank's rows
+                draw = self._rng.standard_normal(part.n)[part.r0:part.r1]
+            v = _dev.to_device_block(draw.reshape(-1, 1))
             for _pass in range(2):
                 project_chain(v, v, bases, [s[: b.shape[1]] for s, b in zip(scratch, bases)])
             ss = torch.zeros(1, dtype=torch.float64, device=self.device)

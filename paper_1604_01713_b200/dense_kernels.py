@@ -112,10 +112,36 @@ def cholqr2_finish(host_buf: np.ndarray, host_status: np.ndarray, L: int):
 
 
 def tsqr_into(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch) -> None:
-    """Householder TSQR of X into Q (copying first when they differ)."""
+    """Householder TSQR of X into Q (copying first when they differ).
+
+    Row-partitioned: each rank factors its rows, the ranks' R factors are
+    all-gathered, the stack is factored on every rank (identical input,
+    identical LAPACK result), and each rank applies its block of the small Q
+    to its rows (Q_local <- Q_local S_rank, one rg_tall pass)."""
     if Q.data_ptr() != X.data_ptr():
         Q.copy_(X)
     _dev.tsqr(Q, scr.RT)
+    comm = _dev.get_comm()
+    if comm is None or comm.world == 1:
+        return
+    L = Q.shape[1]
+    S_rank, rs = tsqr_combine(np.triu(scr.RT.cpu().numpy()), comm)
+    S = torch.from_numpy(S_rank).to(Q.device)
+    _dev.tall(None, Q, [(Q, S, 1.0)], n=Q.shape[0], p=L)
+    scr.RT.copy_(torch.from_numpy(np.asfortranarray(rs)).to(Q.device))
+
+
+def tsqr_combine(R_local: np.ndarray, comm):
+    """Top level of the distributed TSQR: QR of the all-gathered R factors
+    (identical on every rank), sign-fixed to r_jj >= 0.  Returns this rank's
+    L x L block of the small Q and the global R."""
+    L = R_local.shape[1]
+    stack = np.vstack(comm.allgather_np(R_local))
+    qs, rs = np.linalg.qr(stack, mode="reduced")
+    s = np.where(np.diagonal(rs) < 0.0, -1.0, 1.0)
+    qs = qs * s
+    rs = rs * s[:, None]
+    return np.asfortranarray(qs[comm.rank * L:(comm.rank + 1) * L]), rs
 
 
 def reduced_qr_device(X: torch.Tensor, rank_tol: float = 1e-12, Q: torch.Tensor | None = None,

@@ -23,6 +23,25 @@ MAX_GC = 128      # Gram basis columns per launch
 MAX_TERM_COLS = 512
 
 
+_COMM = None   # distributed.CommContext when row-partitioned (Gram allreduce)
+_PART = None   # distributed.RowPartition of this rank
+
+
+def set_comm(comm, part) -> None:
+    """Register the row-partition context: every Gram / norm rg_tall
+    produces is then summed across ranks."""
+    global _COMM, _PART
+    _COMM, _PART = comm, part
+
+
+def get_comm():
+    return _COMM
+
+
+def get_part():
+    return _PART
+
+
 class NoDeviceError(RuntimeError):
     """The B200 path needs a CUDA device; there is no CPU fallback."""
 
@@ -255,6 +274,8 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
         _t1(e0, label, esz * n * cols)
     if gout_k is not gout:
         gout.copy_(gout_k)
+    if gmode and _COMM is not None:
+        _COMM.allreduce_(gout)
 
 
 def _dense_f(t: torch.Tensor) -> bool:

@@ -1,0 +1,333 @@
+"""Row-partitioned multi-GPU execution (one process per GPU).
+
+The reference is single-process; this is the B200 build's
+scaling layer:
+
+* ``RowPartition``   contiguous row blocks [r0, r1) of A, B, X, R, W, C, U
+                     (optionally aligned to whole grid planes).
+* ``HaloPlan``       for the local rows of A: the columns owned by other
+                     ranks ("ghosts"), grouped by owner in ascending global
+                     order, and the rows this rank must send to each peer
+                     (recv lists exchanged once with all_gather_object).
+                     The local CSR keeps every row's entries in their
+                     original (ascending global column) order and only
+                     renumbers the column indices: owned j -> j - r0, ghost
+                     j -> n_local + slot.  The SpMM therefore performs the
+                     reference's exact per-row operation sequence and stays
+                     bitwise equal to the single-GPU product.
+* ``DistCsr``        the operator: per application, pack the send rows,
+                     exchange them (NCCL isend/irecv, or host-staged for
+                     gloo), run the interior rows (no ghost columns) while
+                     the exchange is in flight, then the boundary rows.
+* ``CommContext``    the sum-allreduce applied to every Gram / norm that
+                     rg_tall produces (device.set_comm); the (k+mp) x p
+                     Grams are a few KB, i.e. latency-bound.
+
+Host-side small problems (progressive LS, harmonic Ritz) are replicated on
+every rank from bitwise-identical allreduced inputs.  Seeded random vectors
+(breakdown repair, block enlargement) are drawn at the global size on every
+rank and sliced, so they equal the single-process draws.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import device as _dev
+
+
+# ---------------------------------------------------------------------------
+# partition
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class RowPartition:
+    n: int
+    world: int
+    rank: int
+    bounds: np.ndarray  # world + 1 row offsets
+
+    @classmethod
+    def even(cls, n: int, world: int, rank: int, align: int = 1) -> "RowPartition":
+        """Contiguous blocks of (as nearly as possible) equal size, cut at
+        multiples of ``align`` rows (e.g. one z-plane of a stencil)."""
+        units = (n + align - 1) // align
+        cuts = [min(n, (units * q // world) * align) for q in range(world + 1)]
+        cuts[-1] = n
+        return cls(n, world, rank, np.asarray(cuts, dtype=np.int64))
+
+    @property
+    def r0(self) -> int:
+        return int(self.bounds[self.rank])
+
+    @property
+    def r1(self) -> int:
+        return int(self.bounds[self.rank + 1])
+
+    @property
+    def n_local(self) -> int:
+        return self.r1 - self.r0
+
+    def owner(self, cols: np.ndarray) -> np.ndarray:
+        return np.searchsorted(self.bounds, cols, side="right") - 1
+
+
+# ---------------------------------------------------------------------------
+# halo plan
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class HaloPlan:
+    part: RowPartition
+    row_ptr: np.ndarray           # local CSR (n_local + 1)
+    col_idx: np.ndarray           # renumbered columns
+    values: np.ndarray
+    ghost_cols: np.ndarray        # global ids of ghost slots, ascending
+    recv_ranges: dict             # peer -> (slot0, slot1)
+    send_rows: dict = field(default_factory=dict)  # peer -> local row ids to send
+    interior: tuple = (0, 0)      # [i0, i1): rows without ghost columns
+
+    @property
+    def n_ghost(self) -> int:
+        return int(self.ghost_cols.size)
+
+    @classmethod
+    def from_local_rows(cls, part: RowPartition, row_ptr, col_idx, values, exchange=None) -> "HaloPlan":
+        """Build from the local rows (global column indices, ascending per
+        row).  ``exchange(recv_lists) -> {peer: rows peer needs from me}``
+        defaults to all_gather_object over the default process group."""
+        rp = np.asarray(row_ptr, dtype=np.int64)
+        ci = np.asarray(col_idx, dtype=np.int64)
+        r0, r1 = part.r0, part.r1
+        owned = (ci >= r0) & (ci < r1)
+        ghosts = np.unique(ci[~owned])
+        slot = np.searchsorted(ghosts, ci[~owned])
+        new_ci = ci.copy()
+        new_ci[owned] -= r0
+        new_ci[~owned] = part.n_local + slot
+        owners = part.owner(ghosts)
+        recv_ranges = {}
+        recv_lists = {}
+        for q in np.unique(owners):
+            idx = np.flatnonzero(owners == q)
+            recv_ranges[int(q)] = (int(idx[0]), int(idx[-1]) + 1)
+            recv_lists[int(q)] = ghosts[idx]
+        # interior rows: the longest middle range whose rows touch no ghost
+        nl = part.n_local
+        row_has_ghost = np.zeros(nl, dtype=bool)
+        if (~owned).any():
+            rows = np.repeat(np.arange(nl), np.diff(rp))
+            row_has_ghost[np.unique(rows[~owned])] = True
+        if row_has_ghost.any():
+            g = np.flatnonzero(row_has_ghost)
+            # boundary rows form a prefix and a suffix for slab partitions
+            first_gap = np.flatnonzero(np.diff(g) > 1)
+            if first_gap.size:
+                i0 = int(g[first_gap[0]]) + 1
+                i1 = int(g[first_gap[0] + 1])
+            elif g[0] == 0:
+                i0, i1 = int(g[-1]) + 1, nl
+            elif g[-1] == nl - 1:
+                i0, i1 = 0, int(g[0])
+            else:
+                i0 = i1 = 0
+        else:
+            i0, i1 = 0, nl
+        plan = cls(part, rp.astype(np.int32), new_ci.astype(np.int32), np.asarray(values),
+                   ghosts, recv_ranges, {}, (i0, i1))
+        ex = exchange if exchange is not None else _exchange_recv_lists
+        needed_from_me = ex(part, recv_lists)
+        plan.send_rows = {q: (np.asarray(g_ids, dtype=np.int64) - r0) for q, g_ids in needed_from_me.items()}
+        return plan
+
+
+def _exchange_recv_lists(part: RowPartition, recv_lists: dict) -> dict:
+    gathered = [None] * part.world
+    dist.all_gather_object(gathered, {q: v.tolist() for q, v in recv_lists.items()})
+    out = {}
+    for q, lists in enumerate(gathered):
+        if q == part.rank or lists is None:
+            continue
+        mine = lists.get(part.rank)
+        if mine:
+            out[q] = np.asarray(mine, dtype=np.int64)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# communicator context (Gram allreduce + halo exchange transport)
+# ---------------------------------------------------------------------------
+
+
+class CommContext:
+    """Sum-allreduce of Grams and point-to-point halo transport over a
+    torch.distributed group.  NCCL moves CUDA buffers directly (NVLink);
+    other backends (gloo, used by the CPU tests) stage through host memory."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nccl = dist.get_backend(group) == "nccl"
+
+    def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world == 1:
+            return t
+        if self.nccl or not t.is_cuda:
+            buf = t if t.is_contiguous() else t.contiguous()
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+            if buf is not t:
+                t.copy_(buf)
+            return t
+        h = t.detach().cpu().contiguous()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+        t.copy_(h)
+        return t
+
+    def exchange(self, sends: dict, recvs: dict):
+        """Post all sends/recvs; returns a list of works (wait() on each)."""
+        ops = []
+        staged = []
+        for q, buf in recvs.items():
+            if self.nccl or not buf.is_cuda:
+                ops.append(dist.P2POp(dist.irecv, buf, q, self.group))
+            else:
+                h = torch.empty(buf.shape, dtype=buf.dtype)
+                staged.append((buf, h))
+                ops.append(dist.P2POp(dist.irecv, h, q, self.group))
+        for q, buf in sends.items():
+            if self.nccl or not buf.is_cuda:
+                ops.append(dist.P2POp(dist.isend, buf, q, self.group))
+            else:
+                ops.append(dist.P2POp(dist.isend, buf.cpu(), q, self.group))
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return works, staged
+
+    def allgather_np(self, arr: np.ndarray) -> list:
+        """All ranks' copies of a small host array (same shape everywhere)."""
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if self.nccl:
+            t = t.cuda()
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+    @staticmethod
+    def finish(works, staged):
+        for w in works:
+            w.wait()
+        for dst, h in staged:
+            dst.copy_(h)
+
+
+# ---------------------------------------------------------------------------
+# distributed operator
+# ---------------------------------------------------------------------------
+
+
+class DistCsr:
+    """Row block of A on this rank + its halo plan; ``apply_into`` is the
+    distributed A @ Z for column-major local blocks Z (n_local x p)."""
+
+    def __init__(self, plan: HaloPlan, comm: CommContext, device=None, local_spmm=None):
+        self.plan = plan
+        self.part = plan.part
+        self.comm = comm
+        self.n_rows = self.part.n_local
+        self.n_cols = self.part.n_local
+        self.n_global = self.part.n
+        self.device = device
+        self._local_spmm = local_spmm
+        if local_spmm is None:
+            from .sparse_core import DeviceCsr
+
+            self.dcsr = DeviceCsr.from_host(self.n_rows, self.n_rows + plan.n_ghost, plan.row_ptr, plan.col_idx,
+                                            plan.values, device)
+            dev = self.dcsr.device
+        else:
+            self.dcsr = None
+            dev = torch.device("cpu") if device is None else torch.device(device)
+        self.dev = dev
+        self._send_idx = {q: torch.from_numpy(v).to(dev) for q, v in plan.send_rows.items()}
+        self._ghost = {}
+
+    def _ghost_block(self, p, dtype):
+        key = (p, dtype)
+        if key not in self._ghost:
+            ng = max(self.plan.n_ghost, 1)
+            # (p, n_ghost) contiguous == column-major (n_ghost, p), ld = n_ghost
+            self._ghost[key] = torch.zeros((p, ng), dtype=dtype, device=self.dev)
+        return self._ghost[key]
+
+    def apply_into(self, Z: torch.Tensor, out: torch.Tensor) -> None:
+        plan = self.plan
+        p = Z.shape[1]
+        G = self._ghost_block(p, Z.dtype)
+        # pack: rows each peer needs, as (p, k) contiguous blocks
+        sends = {q: Z.index_select(0, idx).t().contiguous() for q, idx in self._send_idx.items()}
+        recvs = {q: torch.empty((p, s1 - s0), dtype=Z.dtype, device=self.dev)
+                 for q, (s0, s1) in plan.recv_ranges.items()}
+        works, staged = self.comm.exchange(sends, recvs) if self.comm is not None else ([], [])
+        i0, i1 = plan.interior
+        # interior rows need no ghost column: overlap them with the exchange
+        if i1 > i0:
+            self._spmm(Z, out, i0, i1, None)
+        CommContext.finish(works, staged)
+        for q, (s0, s1) in plan.recv_ranges.items():
+            G[:, s0:s1].copy_(recvs[q])
+        Xg = G.t()[: plan.n_ghost] if plan.n_ghost else None
+        if i0 > 0:
+            self._spmm(Z, out, 0, i0, Xg)
+        if i1 < self.n_rows:
+            self._spmm(Z, out, max(i1, i0), self.n_rows, Xg)
+
+    def _spmm(self, Z, out, rb, re, Xg):
+        if self._local_spmm is not None:
+            self._local_spmm(self.plan, Z, out, rb, re, Xg)
+            return
+        _dev.spmm(self.dcsr, Z, out, rb, re, n_local=self.n_rows, Xg=Xg)
+
+    # solver integration
+    def __call__(self, Z):
+        out = _dev.empty_block(Z.shape[0], Z.shape[1], Z.device, Z.dtype)
+        self.apply_into(Z, out)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def local_rows(part: RowPartition, M):
+    """Rows [r0, r1) of a host block / CsrMatrix-like array."""
+    return M[part.r0: part.r1]
+
+
+def csr_row_block(row_ptr, col_idx, values, r0, r1):
+    """CSR arrays of rows [r0, r1) (global column indices)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    a, b = rp[r0], rp[r1]
+    return rp[r0: r1 + 1] - a, np.asarray(col_idx)[a:b], np.asarray(values)[a:b]
+
+
+def setup(A, group=None, align: int = 1, device=None):
+    """Partition a host CsrMatrix across the ranks of ``group`` and register
+    the Gram allreduce.  Returns (DistCsr, RowPartition)."""
+    comm = CommContext(group)
+    part = RowPartition.even(A.n_rows, comm.world, comm.rank, align)
+    rp, ci, v = csr_row_block(A.row_ptr, A.col_idx, A.values, part.r0, part.r1)
+    plan = HaloPlan.from_local_rows(part, rp, ci, v)
+    op = DistCsr(plan, comm, device)
+    _dev.set_comm(comm, part)
+    return op, part
+
+
+def teardown():
+    _dev.set_comm(None, None)

@@ -22,11 +22,14 @@ import torch
 from . import device as _dev
 
 
-def project_chain(zin: torch.Tensor, zbuf: torch.Tensor, bases, coefs, tail_gram=None):
+def project_chain(zin: torch.Tensor, zbuf: torch.Tensor, bases, coefs, tail_gram=None, tall=None):
     """z = zin projected sequentially against ``bases``; the final z lands in
     ``zbuf`` (which may alias zin); coefs[i] (device, a_i x p, column-major)
     receives B_i^T z_{i}.  ``tail_gram`` (e.g. ("self", G)) is fused into the
-    final pass.  Returns the number of passes launched."""
+    final pass.  ``tall`` defaults to the rg_tall wrapper (tests substitute a
+    host restatement to exercise the schedule without a GPU).  Returns the
+    number of passes launched."""
+    tall = _dev.tall if tall is None else tall
     p = zin.shape[1]
     pending = []  # (B, coef) updates not yet folded into the stored z
     cur = zin
@@ -42,15 +45,15 @@ def project_chain(zin: torch.Tensor, zbuf: torch.Tensor, bases, coefs, tail_gram
         store = len(pending) + 1 > 2 or carry_cols > p
         terms = [(b, c, -1.0) for b, c in pending]
         if store:
-            _dev.tall(cur, zbuf, terms, gram=("basis", B, coefs[i]))
+            tall(cur, zbuf, terms, gram=("basis", B, coefs[i]))
             cur = zbuf
             pending = []
         else:
-            _dev.tall(cur, None, terms, gram=("basis", B, coefs[i]))
+            tall(cur, None, terms, gram=("basis", B, coefs[i]))
         pending.append((B, coefs[i]))
         launches += 1
     terms = [(b, c, -1.0) for b, c in pending]
     if terms or tail_gram is not None or cur.data_ptr() != zbuf.data_ptr():
-        _dev.tall(cur, zbuf, terms, gram=tail_gram)
+        tall(cur, zbuf, terms, gram=tail_gram)
         launches += 1
     return launches
