@@ -82,7 +82,7 @@ class ClockSampler:
                     self.samples.append(parts)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._th = threading.Thread(target=self._run, daemon=True)
@@ -168,8 +168,13 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 
 
-def _setup_step(grid, dev, seed=0):
-    """Operator, recycle space and a 9-step factorisation resident on `dev`."""
+def _setup_step(grid, dev, seed=0, world=1, rank=0):
+    """Operator, recycle space and a 9-step factorisation resident on `dev`.
+
+    world > 1: weak scaling -- rank r owns z-planes [r*grid, (r+1)*grid) of a
+    grid x grid x (grid*world) conv-diff operator (2^24 rows per rank at
+    grid=256), with the halo exchange and Gram allreduces of the row
+    partition (paper_1604_01713_b200.distributed)."""
     import torch
 
     from paper_1604_01713_b200 import arnoldi, problems
@@ -178,10 +183,22 @@ def _setup_step(grid, dev, seed=0):
     from paper_1604_01713_b200.solver import _Operator, _scrub
 
     t0 = time.perf_counter()
-    A = problems.conv_diff_3d(grid, 20.0)
+    if world == 1:
+        A = problems.conv_diff_3d(grid, 20.0)
+        op = _Operator(A, None, "none")
+        n, nnz = A.n_rows, A.nnz
+    else:
+        from paper_1604_01713_b200 import distributed as DI
+
+        rp, ci, v, n_glob = problems.conv_diff_3d_slab(grid, grid * world, 20.0, rank * grid, (rank + 1) * grid)
+        comm = DI.CommContext()
+        part = DI.RowPartition.even(n_glob, world, rank, align=grid * grid)
+        plan = DI.HaloPlan.from_local_rows(part, rp, ci, v)
+        dop = DI.DistCsr(plan, comm, dev)
+        D.set_comm(comm, part)
+        op = _Operator(dop, None, "none")
+        n, nnz = part.n_local, len(v)
     t_gen = time.perf_counter() - t0
-    n = A.n_rows
-    op = _Operator(A, None, "none")
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     U0 = D.empty_block(n, K_RECYCLE, dev)
@@ -194,7 +211,7 @@ def _setup_step(grid, dev, seed=0):
     for _ in range(M_STEPS - 1):
         arnoldi.step(fact, op.apply, recycle=rs)
     torch.cuda.synchronize()
-    return A, op, rs, fact, t_gen
+    return (n, nnz), op, rs, fact, t_gen
 
 
 def _one_step(fact, op, rs):
@@ -209,14 +226,13 @@ def run_ours(args, rank, world):
 
     from paper_1604_01713_b200 import device as D
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-    A, op, rs, fact, t_gen = _setup_step(args.grid, dev, seed=rank)
-    n, nnz = A.n_rows, A.nnz
+    (n, nnz), op, rs, fact, t_gen = _setup_step(args.grid, dev, seed=rank, world=world, rank=rank)
     model_bytes, parts = step_model_bytes(n, nnz)
 
     for _ in range(args.warmup):
@@ -258,6 +274,15 @@ def run_ours(args, rank, world):
     e2e = None
     if not args.no_e2e:
         e2e = _e2e(fact, op, rs, model_bytes, args, dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([e2e["ms_per_step"]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e["ms_per_step"] = float(t.item())
+            e2e["value"] = model_bytes * world / (e2e["ms_per_step"] * 1e-3) / 1e9
+            e2e["h2d_bytes_per_step"] *= world
+            e2e["d2h_bytes_per_step"] *= world
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -269,8 +294,8 @@ def run_ours(args, rank, world):
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"cfg4-step: arnoldi.step #10 of a cycle, {args.grid}^3 conv-diff beta=20, "
-                                       f"n={n}, nnz={nnz}, p=8, k=20, basis 80 cols (cfg3 shapes)",
+                "config": {"workload": f"cfg4-step: arnoldi.step #10 of a cycle, {args.grid}^3 conv-diff beta=20 "
+                                       f"per GPU, n={n}, nnz={nnz} per GPU, p=8, k=20, basis 80 cols (cfg3 shapes)",
                            "model_bytes_per_step": model_bytes, "model_parts": parts,
                            "l2": "inputs (>14 GB) far larger than the 126 MB L2; no flush needed",
                            "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU"},
@@ -322,7 +347,7 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--grid", type=int, default=256)
@@ -339,8 +364,9 @@ def main():
         else:
             import torch
 
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-            dist.init_process_group("nccl")
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1))
+            # RG_BENCH_BACKEND=gloo runs the N>1 code path on a single GPU (test only)
+            dist.init_process_group(os.environ.get("RG_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

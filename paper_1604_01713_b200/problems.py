@@ -60,6 +60,40 @@ def _stencil_csr(N: int, dim: int, diag_val: float, off_lo: float, off_hi: float
     return CsrMatrix(n, n, row_ptr.astype(np.int32), col_idx, values, _validated=True)
 
 
+def conv_diff_3d_slab(N: int, Nz: int, beta: float, z0: int, z1: int):
+    """Rows of z-planes [z0, z1) of the 7-point conv-diff operator on an
+    N x N x Nz grid (h = 1/(N+1) in every direction, same coefficients as
+    conv_diff_3d), with GLOBAL column indices.  Used by the weak-scaling
+    bench: each rank generates only its slab.  Returns (row_ptr, col_idx,
+    values, n_global)."""
+    h = 1.0 / (N + 1)
+    h2 = h**2
+    t_off = -1.0 / h2
+    t_diag = 2.0 / h2
+    d = 1.0 / (2 * h)
+    diag = (t_diag + t_diag) + t_diag
+    lo, hi = t_off + beta * (-d), t_off + beta * d
+    plane = N * N
+    n_global = plane * Nz
+    idx = np.arange(z0 * plane, z1 * plane, dtype=np.int64)
+    x, y, z = idx % N, (idx // N) % N, idx // plane
+    offs = [(-plane, z > 0, lo), (-N, y > 0, lo), (-1, x > 0, lo), (0, None, diag),
+            (1, x < N - 1, hi), (N, y < N - 1, hi), (plane, z < Nz - 1, hi)]
+    nl = idx.size
+    cols = np.empty((nl, 7), dtype=np.int64)
+    vals = np.empty((nl, 7), dtype=np.float64)
+    keep = np.ones((nl, 7), dtype=bool)
+    for s, (o, ok, v) in enumerate(offs):
+        cols[:, s] = idx + o
+        vals[:, s] = v
+        if ok is not None:
+            keep[:, s] = ok
+    counts = keep.sum(axis=1)
+    row_ptr = np.zeros(nl + 1, dtype=np.int64)
+    np.cumsum(counts, out=row_ptr[1:])
+    return row_ptr, cols[keep], vals[keep], n_global
+
+
 def conv_diff_2d(N: int, beta: float) -> CsrMatrix:
     """-Lap u + beta (u_x + u_y), 5-point central FD on an N x N interior grid,
     h = 1/(N+1), Dirichlet eliminated (BASELINE configs[0]: N=64, beta=10)."""

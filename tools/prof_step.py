@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    A, op, rs, fact, _ = bench._setup_step(args.grid, dev)
+    _, op, rs, fact, _ = bench._setup_step(args.grid, dev)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     for _ in range(args.steps):
