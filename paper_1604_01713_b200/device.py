@@ -268,7 +268,11 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
     _lib.check(rc, "tall")
     if n > 0 or gmode:
         esz = 16 if cplx else 8
-        cols = (p if zin is not None else 0) + a1 + a2 + (gc if gmode == 1 else 0) + (p if zout is not None else 0)
+        # a Gram basis that aliases an update operand is streamed once
+        aliased = gmode == 1 and any(x is not None and x.data_ptr() == gb.data_ptr() and gc <= x.shape[1]
+                                     for x in (x1, x2))
+        cols = ((p if zin is not None else 0) + a1 + a2 + (gc if gmode == 1 and not aliased else 0)
+                + (p if zout is not None and (zin is None or zout.data_ptr() != zin.data_ptr()) else p if zout is not None else 0))
         label = (f"rg_tall p={p} in={int(zin is not None)} a={a1}+{a2} "
                  f"g{gmode}:{gc} trsm={int(r1 is not None) + int(r2 is not None)} out={int(zout is not None)}")
         _t1(e0, label, esz * n * cols)
