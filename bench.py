@@ -344,6 +344,87 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
             "path": "arnoldi.step with basis/C uploaded from pinned host memory and V_11 downloaded each step"}
 
 
+# ---------------------------------------------------------------------------
+# time-to-solution workload (BASELINE configs[3]: "GCRO-DR solve s/system")
+# ---------------------------------------------------------------------------
+
+
+def run_solve(args, rank, world):
+    """Full block GCRO-DR sequence of the config-4 family (3-D conv-diff
+    grid^3, beta=20, p=8, m=10, k=20, tol 1e-8, `--systems` systems with the
+    0.5 %*i*u*diag(A) perturbations).  Strong scaling over `world` GPUs: the
+    same global problem is row-partitioned on whole z-planes."""
+    import torch
+
+    from paper_1604_01713_b200 import SolverConfig, problems, solve_block_gcrodr
+    from paper_1604_01713_b200 import device as D
+
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    grid, nsys = args.grid, args.systems
+    t0 = time.perf_counter()
+    n_glob = grid ** 3
+    B = np.asfortranarray(np.random.default_rng(0).standard_normal((n_glob, P_BLOCK)))
+    u = np.random.default_rng(1).uniform(0.0, 1.0, n_glob)
+    if world == 1:
+        A, _, system, kw = problems.cfg4_sequence(N=grid, n_systems=nsys)
+        ops = [system(i) for i in range(nsys)]
+        part = None
+    else:
+        from paper_1604_01713_b200 import distributed as DI
+        from paper_1604_01713_b200.problems import add_diagonal  # noqa: F401
+
+        comm = DI.CommContext()
+        part = DI.RowPartition.even(n_glob, world, rank, align=grid * grid)
+        z0, z1 = part.r0 // (grid * grid), part.r1 // (grid * grid)
+        rp, ci, v, _ = problems.conv_diff_3d_slab(grid, grid, 20.0, z0, z1)
+        rows = np.repeat(np.arange(part.n_local), np.diff(rp))
+        on_diag = ci == rows + part.r0
+        ops = []
+        for i in range(nsys):
+            vi = v.copy()
+            if i:
+                dA = v[on_diag]
+                vi[on_diag] = dA + 0.005 * i * u[part.r0:part.r1] * dA
+            plan = DI.HaloPlan.from_local_rows(part, rp, ci, vi)
+            ops.append(DI.DistCsr(plan, comm, dev))
+        D.set_comm(comm, part)
+        kw = dict(m=10, k=20, tol=1e-8, max_cycles=200)
+    t_setup = time.perf_counter() - t0
+    cfg = SolverConfig(**kw)
+    rs = None
+    per = []
+    for i, Ai in enumerate(ops):
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        X, rep, rs_out = solve_block_gcrodr(Ai, B, None, cfg, rs_in=rs)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t1
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        rs = rs_out if rs_out is not None else rs
+        per.append({"system": i, "s": dt, "cycles": rep.cycles, "block_steps": int(sum(len(h) for h in rep.residual_history)),
+                    "matvecs": rep.matvec_count, "converged": bool(rep.converged),
+                    "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms))})
+    if rank == 0:
+        mean = statistics.mean(r["s"] for r in per)
+        line = {"metric": "GCRO-DR solve s/system (cfg4 family)", "value": mean, "unit": "s/system",
+                "n_gpus": world, "steps": nsys, "warmup": 0, "ms_per_step": mean * 1e3,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": {"workload": f"cfg4 sequence {grid}^3 conv-diff beta=20, p=8, m=10, "
+                                                            f"k=20, tol 1e-8, {nsys} systems",
+                                                "setup_s": t_setup, "parallelism": f"row-partition x{world}"},
+                "systems": per}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -353,6 +434,8 @@ def main():
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", choices=["step", "solve"], default="step")
+    ap.add_argument("--systems", type=int, default=5)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -369,6 +452,8 @@ def main():
             dist.init_process_group(os.environ.get("RG_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "solve":
+        run_solve(args, rank, world)
     else:
         run_ours(args, rank, world)
     if world > 1:
