@@ -144,6 +144,38 @@ def tsqr_combine(R_local: np.ndarray, comm):
     return np.asfortranarray(qs[comm.rank * L:(comm.rank + 1) * L]), rs
 
 
+TSQR_MAX_P = 32
+
+
+def _wide_qr(X: torch.Tensor, Q: torch.Tensor, rank_tol: float) -> QrFactors:
+    """Thin QR of a block wider than TSQR_MAX_P columns: column panels of
+    32, each made orthogonal to the previous panels by block CGS2 (fused
+    projection passes) and then factored by Householder TSQR.  R collects the
+    projection coefficients above the diagonal blocks."""
+    n, L = X.shape
+    if Q.data_ptr() != X.data_ptr():
+        Q.copy_(X)
+    ss = torch.zeros(L, dtype=torch.float64, device=X.device)
+    _dev.tall(Q, None, gram=("sumsq", ss))
+    norm_x = float(np.sqrt(ss.sum().item()))
+    R = np.zeros((L, L))
+    from .ortho import project_chain
+
+    for b0 in range(0, L, TSQR_MAX_P):
+        b1 = min(L, b0 + TSQR_MAX_P)
+        Qb = Q[:, b0:b1]
+        if b0:
+            prev = Q[:, :b0]
+            c1, c2 = _dev.small(b0, b1 - b0, X.device), _dev.small(b0, b1 - b0, X.device)
+            project_chain(Qb, Qb, [prev, prev], [c1, c2])
+            R[:b0, b0:b1] = c1.cpu().numpy() + c2.cpu().numpy()
+        scr = QrScratch(b1 - b0, X.device)
+        tsqr_into(Qb, Qb, scr)
+        R[b0:b1, b0:b1] = np.triu(scr.RT.cpu().numpy())
+    flagged = _flags(R, norm_x, rank_tol)
+    return QrFactors(q=Q, r_factor=R, rank=int(L - flagged.sum()), flagged=flagged)
+
+
 def reduced_qr_device(X: torch.Tensor, rank_tol: float = 1e-12, Q: torch.Tensor | None = None,
                       scr: QrScratch | None = None) -> QrFactors:
     """Device thin QR; X is not modified (unless Q is X)."""
@@ -153,6 +185,8 @@ def reduced_qr_device(X: torch.Tensor, rank_tol: float = 1e-12, Q: torch.Tensor 
     dev = X.device
     if Q is None:
         Q = _dev.empty_block(n, L, dev)
+    if L > TSQR_MAX_P:
+        return _wide_qr(X, Q, rank_tol)
     if scr is None or scr.L != L:
         scr = QrScratch(L, dev)
     in_place = Q.data_ptr() == X.data_ptr()

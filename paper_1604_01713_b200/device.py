@@ -46,21 +46,31 @@ class NoDeviceError(RuntimeError):
     """The B200 path needs a CUDA device; there is no CPU fallback."""
 
 
+_CUDA_OK = None
+
+
 def require_cuda(device=None) -> torch.device:
-    if not torch.cuda.is_available():
+    global _CUDA_OK
+    if _CUDA_OK is None:
+        _CUDA_OK = torch.cuda.is_available()
+    if not _CUDA_OK:
         raise NoDeviceError("paper_1604_01713_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if device is None:
+        return torch.device("cuda", torch._C._cuda_getDevice())
+    dev = device if isinstance(device, torch.device) else torch.device(device)
     if dev.type != "cuda":
         raise NoDeviceError(f"device {dev} is not a CUDA device")
     return dev
 
 
 def lib():
-    return _lib.load()
+    return _lib._lib if _lib._lib is not None else _lib.load()
 
 
 def stream_ptr() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """Raw handle of torch's current stream on the current device (the
+    launch stream of every rg_* call)."""
+    return torch._C._cuda_getCurrentRawStream(torch._C._cuda_getDevice())
 
 
 def round_ld(n: int) -> int:

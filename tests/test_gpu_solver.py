@@ -171,3 +171,28 @@ def test_recycling_golden(cuda):
     U3, C3 = rs3.numpy()
     assert np.abs(C3 - g["cross/C"]).max() <= 1e-10
     assert np.abs(U3 - g["cross/U"]).max() <= 1e-9 * np.abs(g["cross/U"]).max()
+
+
+def test_cfg4_family_64_sequence_matches_reference(cuda):
+    """BASELINE configs[3] family at 64^3 (n = 262,144; p=8, m=10, k=20,
+    5 systems): the reference's golden run (448 s on 8 CPU cores) and the
+    device run must agree on every system's cycles, block steps and matvec
+    counts, with residual histories within 1e-8 ||B||_F (the handed-over
+    recycle space amplifies rounding differences along the sequence: the
+    first systems agree to 1e-9, the fifth to ~2.4e-9)."""
+    from paper_1604_01713_b200 import SolverConfig, problems, solve_sequence
+
+    g = load_golden("cfg4_64_cases.npz")
+    A, B, system, kw = problems.cfg4_sequence(N=64, n_systems=5)
+    reps = solve_sequence([(system(i), B) for i in range(5)], SolverConfig(**kw))
+    bnorm = np.linalg.norm(B)
+    for i, rep in enumerate(reps):
+        pre = f"sys{i}/"
+        assert rep.error is None, rep.error
+        assert rep.cycles == int(g[pre + "cycles"]), (i, rep.cycles)
+        assert [len(h) for h in rep.residual_history] == g[pre + "steps"].tolist(), i
+        assert rep.matvec_count == int(g[pre + "matvecs"]), i
+        assert rep.converged == bool(g[pre + "converged"])
+        hist = np.concatenate(rep.residual_history, axis=0)
+        assert np.abs(hist - g[pre + "hist"]).max() <= 1e-8 * bnorm, i
+        assert np.allclose(np.linalg.norm(rep.solution, axis=0), g[pre + "Xnorms"], rtol=1e-8)

@@ -2,6 +2,7 @@
 reference (tests/golden/make_golden.py) — CPU only."""
 
 import numpy as np
+import torch  # noqa: F401
 
 import oracle
 from conftest import csr_from, load_golden
@@ -55,3 +56,25 @@ def test_oracle_bytes_model_vs_reference():
     assert oracle.spmm_bytes(5, 7, 3) == int(g["matvec_bytes_5_7_3"])
     for p, ref in zip((1, 2, 4, 8, 16), g["matvec_bytes_cfg2"]):
         assert oracle.spmm_bytes(2097152, 14581760, p) == int(ref)
+
+
+def test_bench_module_bytes_model_and_csv(tmp_path):
+    """The device bench module keeps the reference's bytes model and CSV
+    schema (bench.py:44-55, :169-186) — host-only checks."""
+    from paper_1604_01713_b200 import bench as B
+
+    g = load_golden("bench_model.npz")
+    assert B.matvec_bytes(5, 7, 3) == int(g["matvec_bytes_5_7_3"])
+    assert B.projector_bytes(1000, 10, 4, "cgs2") == int(g["projector_bytes_cgs2"])
+    assert B.projector_bytes(1000, 10, 4, "mgs") == int(g["projector_bytes_mgs"])
+    res = [B.BenchResult("m", 10, 30, 2, "all-at-once", "cgs2", 3, 5, 1.5e-3, 1e-3, 2e-4, 999),
+           B.BenchResult("m", 10, 30, 2, "one-at-a-time", "cgs2", 3, 5, 4e-3, 3e-3, 1e-4, 1998)]
+    p = tmp_path / "r.csv"
+    B.emit_csv(res, p)
+    text = p.read_bytes()
+    assert b"\r" not in text and text.splitlines()[0].decode().split(",") == B.CSV_HEADER
+    back = B.read_results_csv(p)
+    assert [(b.matrix_id, b.L, b.mode, b.projector, b.dim_c, b.bytes_model) for b in back] == \
+        [(r.matrix_id, r.L, r.mode, r.projector, r.dim_c, r.bytes_model) for r in res]
+    assert all(abs(b.mean_seconds - r.mean_seconds) <= 1e-6 * r.mean_seconds for b, r in zip(back, res))
+    assert B.block_single_ratios(res)[("m", "cgs2", 3)] == [(2, 1.5e-3 / (4e-3 / 2))]
