@@ -16,8 +16,10 @@
 // gathers X columns; for banded/stencil matrices neighbouring lanes gather
 // neighbouring rows of X, so every X access of the warp is one 256-byte
 // coalesced segment per column.  p accumulators live in registers; wide
-// blocks are processed in column passes of at most 16.
+// blocks are processed in column passes of at most 8.
 #include "rg_common.cuh"
+
+#include <cstdlib>
 
 namespace rg {
 
@@ -115,6 +117,162 @@ spmm_csr_kernel(int64_t row_begin, int64_t row_end,
   }
 }
 
+// ----------------------------------------------------------------------------
+// Persistent variant (production path): warps loop over 32-row units; the
+// CSR entries of the next unit stream into a per-warp double buffer with
+// cp.async while the current unit gathers X, and row_ptr is loaded two units
+// ahead, so a unit's only exposed latency is its X gathers (mostly L2 hits).
+// Units whose 32 rows hold more than kSpmmChunk nonzeros take the chunked
+// synchronous path.  Arithmetic and order are exactly those above.
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+
+struct UnitRp {
+  int32_t wbeg, wend, mybeg, myend;
+};
+
+__device__ __forceinline__ UnitRp load_unit_rp(const int32_t* __restrict__ rp, int64_t wrow0, int64_t row_end,
+                                               int lane) {
+  UnitRp u;
+  const int64_t wlast = min(wrow0 + 32, row_end);
+  const int64_t i = wrow0 + lane;
+  u.wbeg = __ldg(rp + wrow0);
+  u.wend = __ldg(rp + wlast);
+  u.mybeg = i < row_end ? __ldg(rp + i) : 0;
+  u.myend = i < row_end ? __ldg(rp + i + 1) : 0;
+  return u;
+}
+
+template <int PB, bool GHOST>
+__device__ __forceinline__ void accumulate_rows(const int32_t* sci, const double* sva, int lo, int hi,
+                                                const double* __restrict__ X, int64_t ldx, int64_t n_local,
+                                                const double* __restrict__ Xg, int64_t ldg, double (&acc)[PB]) {
+  double xn[PB];
+  double an = 0.0;
+  auto gather = [&](int t, double (&xv)[PB]) {
+    const int64_t j = sci[t];
+    const double* xp = X + j;
+    int64_t ld = ldx;
+    if (GHOST && j >= n_local) {
+      xp = Xg + (j - n_local);
+      ld = ldg;
+    }
+#pragma unroll
+    for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
+  };
+  if (lo < hi) {
+    an = sva[lo];
+    gather(lo, xn);
+  }
+  for (int t = lo; t < hi; ++t) {
+    double xc[PB];
+#pragma unroll
+    for (int c = 0; c < PB; ++c) xc[c] = xn[c];
+    const double ac = an;
+    if (t + 1 < hi) {
+      an = sva[t + 1];
+      gather(t + 1, xn);
+    }
+#pragma unroll
+    for (int c = 0; c < PB; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(ac, xc[c]));
+  }
+}
+
+template <int PB>
+struct SpmmMinBlocks {
+  static constexpr int value = PB >= 16 ? 2 : 3;
+};
+
+template <int PB, bool GHOST>
+__global__ void __launch_bounds__(kSpmmWarps * 32, SpmmMinBlocks<PB>::value)
+spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
+                    const int32_t* __restrict__ ci, const double* __restrict__ va,
+                    const double* __restrict__ X, int64_t ldx, int64_t n_local,
+                    const double* __restrict__ Xg, int64_t ldg, double* __restrict__ Y, int64_t ldy) {
+  __shared__ int32_t s_ci[kSpmmWarps][2][kSpmmChunk];
+  __shared__ double s_va[kSpmmWarps][2][kSpmmChunk];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t nunits = (row_end - row_begin + 31) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * kSpmmWarps;
+  int64_t u = (int64_t)blockIdx.x * kSpmmWarps + w;
+  if (u >= nunits) return;
+
+  auto issue_csr = [&](const UnitRp& r, int buf) {
+    const int32_t cnt = r.wend - r.wbeg;
+    if (cnt <= kSpmmChunk) {
+      for (int e = lane; e < cnt; e += 32) {
+        cp_async4(&s_ci[w][buf][e], ci + r.wbeg + e);
+        cp_async8(&s_va[w][buf][e], va + r.wbeg + e);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+
+  UnitRp cur = load_unit_rp(rp, row_begin + u * 32, row_end, lane);
+  issue_csr(cur, 0);
+  UnitRp nxt = cur;
+  if (u + nwarps < nunits) nxt = load_unit_rp(rp, row_begin + (u + nwarps) * 32, row_end, lane);
+  int buf = 0;
+  for (; u < nunits; u += nwarps) {
+    const bool has_next = u + nwarps < nunits;
+    // CSR of this unit has landed; start the next unit's CSR and row_ptr
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncwarp();
+    if (has_next) issue_csr(nxt, buf ^ 1);
+    UnitRp nn = nxt;
+    if (u + 2 * nwarps < nunits) nn = load_unit_rp(rp, row_begin + (u + 2 * nwarps) * 32, row_end, lane);
+
+    const int64_t wrow0 = row_begin + u * 32;
+    const int64_t i = wrow0 + lane;
+    double acc[PB];
+#pragma unroll
+    for (int c = 0; c < PB; ++c) acc[c] = 0.0;
+    const int32_t cnt = cur.wend - cur.wbeg;
+    if (cnt <= kSpmmChunk) {
+      accumulate_rows<PB, GHOST>(s_ci[w][buf], s_va[w][buf], cur.mybeg - cur.wbeg, cur.myend - cur.wbeg, X, ldx,
+                                 n_local, Xg, ldg, acc);
+    } else {
+      // long rows: chunked synchronous staging through this unit's buffer
+      int32_t* sci = s_ci[w][buf];
+      double* sva = s_va[w][buf];
+      for (int32_t base = cur.wbeg; base < cur.wend; base += kSpmmChunk) {
+        const int32_t c2 = min(kSpmmChunk, cur.wend - base);
+        __syncwarp();
+        for (int e = lane; e < c2; e += 32) {
+          sci[e] = __ldg(ci + base + e);
+          sva[e] = __ldg(va + base + e);
+        }
+        __syncwarp();
+        const int lo = max(cur.mybeg, base) - base;
+        const int hi = min(cur.myend, base + c2) - base;
+        accumulate_rows<PB, GHOST>(sci, sva, lo, hi, X, ldx, n_local, Xg, ldg, acc);
+      }
+    }
+    if (i < row_end) {
+#pragma unroll
+      for (int c = 0; c < PB; ++c) Y[i + c * ldy] = acc[c];
+    }
+    __syncwarp();
+    cur = nxt;
+    nxt = nn;
+    buf ^= 1;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 template <int PB>
 static void launch_spmm(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci,
                         const double* va, const double* X, int64_t ldx, int64_t n_local,
@@ -122,6 +280,28 @@ static void launch_spmm(int64_t rb, int64_t re, const int32_t* rp, const int32_t
   const int64_t rows = re - rb;
   const int64_t rows_per_cta = kSpmmWarps * 32;
   const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
+  if (!getenv("RG_SPMM_LEGACY")) {
+    static int per_sm[2] = {-1, -1};
+    const int gi = Xg ? 1 : 0;
+    if (per_sm[gi] < 0) {
+      int v = 0;
+      if (Xg)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, true>, kSpmmWarps * 32, 0);
+      else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, false>, kSpmmWarps * 32, 0);
+      per_sm[gi] = v < 1 ? 1 : v;
+    }
+    int64_t g = (int64_t)sm_count() * per_sm[gi];
+    if (grid < g) g = grid;
+    if (g < 1) g = 1;
+    if (Xg)
+      spmm_persist_kernel<PB, true><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                          Xg, ldg, Y, ldy);
+    else
+      spmm_persist_kernel<PB, false><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                           Xg, ldg, Y, ldy);
+    return;
+  }
   if (Xg)
     spmm_csr_kernel<PB, true><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
                                                                         Xg, ldg, Y, ldy);
@@ -150,11 +330,12 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
              "rg_spmm_csr_f64: ldx=%lld < n_local=%lld", (long long)ldx, (long long)n_local);
   if (row_end == row_begin) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  // exact-width passes (no per-column predication in the inner loop):
-  // 16-wide passes, then one pass of the remaining width
+  // exact-width passes (no per-column predication in the inner loop) of at
+  // most 8 columns: a 16-wide register block spills, and re-reading A for a
+  // second 8-wide pass is cheaper (profiles/spmm_r01.txt)
   for (int c0 = 0; c0 < p;) {
     const int rem = p - c0;
-    const int pc = rem >= 16 ? 16 : (rem > 8 ? 8 : rem);
+    const int pc = rem >= 8 ? 8 : rem;
     const double* X = d_x ? d_x + (int64_t)c0 * ldx : nullptr;
     const double* Xg = d_xg ? d_xg + (int64_t)c0 * ldg : nullptr;
     double* Y = d_y + (int64_t)c0 * ldy;
