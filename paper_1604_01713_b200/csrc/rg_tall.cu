@@ -833,6 +833,384 @@ static cudaError_t launch_tall(const TallParams& P, size_t smem, int64_t max_gri
 }
 
 
+// ============================================================================
+// v6: every operand through the per-warp cp.async slab ring, DMMA for both
+// the update and the Gram.
+//
+// ncu on v5 (profiles/ncu_step_r01_summary.txt): the update pass with 100
+// operand columns executes ~3.9K warp-instructions per 32-row unit (1 LDG +
+// 8 DFMA + 4 broadcast LDS.128 per column) and sits at ~53% issue
+// utilisation.  Here the unit's slabs are consumed as DMMA m8n8k4 operands:
+//   update   A = X slab (rows x 4 columns, conflict-free stride 36), B = S
+//            fragments pre-arranged in smem, C = the 32x8 z tile in four
+//            row-group fragments: 18 instructions per 8 columns
+//   Gram     A = Gb slab, B = z tile (as v5)
+// The slab cursor walks a per-CTA table of (pointer, ld, valid columns) with
+// increments only, and every stage keeps kRing6-1 slabs in flight.
+// ============================================================================
+
+struct SlabPlan {
+  int nz, n1, n2, ng, total;
+};
+
+constexpr int kV6Warps = 8;
+constexpr int kV6Threads = kV6Warps * 32;
+constexpr int kRing6 = 4;
+constexpr int kSS6 = 36;
+constexpr int kMaxSlabs = 96;
+
+struct SlabTab {
+  const double* ptr[kMaxSlabs];
+  int64_t ld[kMaxSlabs];
+  int nc[kMaxSlabs];
+};
+
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kV6Threads, 2) tall_v6_kernel(TallParams P, SlabPlan L) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  constexpr int MTA = MTMAX > 0 ? MTMAX : 1;
+  constexpr int kWarpWords = kRing6 * 8 * kSS6 + PM8 * kSS6;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ SlabTab tab;
+  const int p = P.p;
+  const int ks1 = (P.a1 + 3) / 4, ks2 = (P.a2 + 3) / 4;
+  double* sf1 = smem;                          // [ks1][NT][32] DMMA B fragments of S1
+  double* sf2 = sf1 + (size_t)ks1 * NT * 32;   // [ks2][NT][32]
+  double* sR1 = sf2 + (size_t)ks2 * NT * 32;   // PM x PM row-major, reciprocal diagonal
+  double* sR2 = sR1 + PM * PM;
+  double* wbase = sR2 + PM * PM;
+  wbase += ((uintptr_t)wbase & 15) ? 1 : 0;
+  double* red = wbase + kV6Warps * kWarpWords;
+
+  for (int e = threadIdx.x; e < ks1 * NT * 32; e += kV6Threads) {
+    const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
+    const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
+    sf1[e] = (aa < P.a1 && c < p) ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
+  }
+  for (int e = threadIdx.x; e < ks2 * NT * 32; e += kV6Threads) {
+    const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
+    const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
+    sf2[e] = (aa < P.a2 && c < p) ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
+  }
+  for (int e = threadIdx.x; e < PM * PM; e += kV6Threads) {
+    const int ii = e / PM, jj = e % PM;
+    const double id = ii == jj ? 1.0 : 0.0;
+    sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
+    sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
+  }
+  for (int k = threadIdx.x; k < L.total; k += kV6Threads) {
+    const double* ptr;
+    int64_t ld;
+    int nc;
+    if (k < L.nz) {
+      ptr = P.zin; ld = P.ldzin; nc = p - k * 8;
+    } else if (k < L.nz + L.n1) {
+      ptr = P.x1; ld = P.ldx1; nc = P.a1 - (k - L.nz) * 8;
+    } else if (k < L.nz + L.n1 + L.n2) {
+      ptr = P.x2; ld = P.ldx2; nc = P.a2 - (k - L.nz - L.n1) * 8;
+    } else {
+      ptr = P.gb; ld = P.ldgb; nc = P.gc - (k - L.nz - L.n1 - L.n2) * 8;
+    }
+    const int s = k < L.nz ? k : (k < L.nz + L.n1 ? k - L.nz : (k < L.nz + L.n1 + L.n2 ? k - L.nz - L.n1 : k - L.nz - L.n1 - L.n2));
+    tab.ptr[k] = ptr + (int64_t)(s * 8) * ld;
+    tab.ld[k] = ld;
+    tab.nc[k] = nc > 8 ? 8 : nc;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  double* ring = wbase + warp * kWarpWords;   // [kRing6][8][kSS6]
+  double* zt = ring + kRing6 * 8 * kSS6;      // [PM8][kSS6]  (column-major tile: zt[c*kSS6 + row])
+  const bool gram_tile = MTMAX > 0 && (P.gmode == 1 || P.gmode == 2);
+  const int mtiles = P.mtiles;
+
+  double acc[MTA][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MTA; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  const int64_t nunits = (P.n + 31) / 32;
+  const int64_t gwarp = (int64_t)blockIdx.x * kV6Warps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kV6Warps;
+  const int64_t my_units = gwarp < nunits ? (nunits - gwarp + nwarps - 1) / nwarps : 0;
+
+  // per-lane chunk geometry: chunk t covers column (lane>>4) + 2t, rows 2*(lane&15) .. +1
+  const int ccol = lane >> 4, rp2 = 2 * (lane & 15);
+  int64_t iss_left = my_units * L.total;
+  int64_t iss_r0 = gwarp * 32;
+  int iss_k = 0, iss_slot = 0;
+  auto issue_next = [&]() {
+    if (iss_left > 0) {
+      const double* base = tab.ptr[iss_k];
+      const int64_t ld = tab.ld[iss_k];
+      const int nc = tab.nc[iss_k];
+      int64_t vr = P.n - (iss_r0 + rp2);
+      vr = vr < 0 ? 0 : (vr > 2 ? 2 : vr);
+      const int rowbytes = (int)vr * 8;
+      const double* src0 = base + iss_r0 + rp2;
+      double* dst0 = ring + iss_slot * 8 * kSS6 + rp2;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = ccol + 2 * t;
+        const int bytes = c < nc ? rowbytes : 0;
+        cp_async16(dst0 + c * kSS6, bytes ? src0 + (int64_t)c * ld : base, bytes);
+      }
+      --iss_left;
+      if (++iss_k == L.total) {
+        iss_k = 0;
+        iss_r0 += nwarps * 32;
+      }
+    }
+    cp_async_commit();
+    if (++iss_slot == kRing6) iss_slot = 0;
+  };
+#pragma unroll
+  for (int s = 0; s < kRing6; ++s) issue_next();
+  int cons_slot = 0;
+  auto acquire = [&]() -> const double* {
+    cp_async_wait<kRing6 - 1>();
+    __syncwarp();
+    const double* s = ring + cons_slot * 8 * kSS6;
+    if (++cons_slot == kRing6) cons_slot = 0;
+    return s;
+  };
+  auto release = [&]() {
+    __syncwarp();
+    issue_next();
+  };
+
+  for (int64_t ui = 0; ui < my_units; ++ui) {
+    const int64_t r0 = (gwarp + ui * nwarps) * 32;
+    // z in DMMA C layout: row group rg (8 rows), lane holds rows rg*8+mrow, cols nt*8 + 2*kq + v
+    double zf[4][NT][2];
+#pragma unroll
+    for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) zf[rg][nt][0] = zf[rg][nt][1] = 0.0;
+    for (int k = 0; k < L.nz; ++k) {
+      const double* sl = acquire();
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        if (h == k) {
+#pragma unroll
+          for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) zf[rg][h][v] = sl[(2 * kq + v) * kSS6 + rg * 8 + mrow];
+        }
+      }
+      release();
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int nsl = t == 0 ? L.n1 : L.n2;
+      if (nsl == 0) continue;
+      const int ksn = t == 0 ? ks1 : ks2;
+      const double* sf = t == 0 ? sf1 : sf2;
+      double m[4][NT][2];
+#pragma unroll
+      for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) m[rg][nt][0] = m[rg][nt][1] = 0.0;
+      for (int s = 0; s < nsl; ++s) {
+        const double* sl = acquire();
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int K = s * 2 + ks;
+          if (K < ksn) {
+            double b[NT];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) b[nt] = sf[(K * NT + nt) * 32 + lane];
+#pragma unroll
+            for (int rg = 0; rg < 4; ++rg) {
+              const double a = sl[(ks * 4 + kq) * kSS6 + rg * 8 + mrow];
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma(m[rg][nt][0], m[rg][nt][1], a, b[nt]);
+            }
+          }
+        }
+        release();
+      }
+      const double alpha = t == 0 ? P.alpha1 : P.alpha2;
+#pragma unroll
+      for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) zf[rg][nt][v] = zf[rg][nt][v] + alpha * m[rg][nt][v];
+    }
+    // ---------------- rows: tile, triangular solves, store, norms
+#pragma unroll
+    for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) zt[(nt * 8 + 2 * kq + v) * kSS6 + rg * 8 + mrow] = zf[rg][nt][v];
+    __syncwarp();
+    const int64_t i = r0 + lane;
+    const bool valid = i < P.n;
+    if (P.r1 || P.r2 || P.zout || P.gmode == 3) {
+      double zr[PM];
+#pragma unroll
+      for (int c = 0; c < PM; ++c) zr[c] = zt[c * kSS6 + lane];
+      if (P.r1 || P.r2) {
+        if (P.r1) trsm_row<PM>(zr, sR1, p);
+        if (P.r2) trsm_row<PM>(zr, sR2, p);
+#pragma unroll
+        for (int c = 0; c < PM; ++c) zt[c * kSS6 + lane] = zr[c];
+      }
+      if (P.zout && valid) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) P.zout[i + (int64_t)c * P.ldzout] = zr[c];
+      }
+      if (P.gmode == 3 && valid) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) sq[c] = fma(zr[c], zr[c], sq[c]);
+      }
+      __syncwarp();
+    }
+    if (!gram_tile) continue;
+    if (P.gmode == 2) {
+#pragma unroll
+      for (int mt = 0; mt < MTA; ++mt) {
+        if (mt < mtiles) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = zt[(mt * 8 + mrow) * kSS6 + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSS6 + ks * 4 + kq]);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int mt = 0; mt < MTA; ++mt) {
+        if (mt < mtiles) {
+          const double* sl = acquire();
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const double a = sl[mrow * kSS6 + ks * 4 + kq];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSS6 + ks * 4 + kq]);
+          }
+          release();
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+
+  // ---------------- epilogue: deterministic reductions
+  __shared__ bool s_last;
+  __syncthreads();
+  if (gram_tile) {
+    for (int ww = 0; ww < kV6Warps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+                red[idx] = (ww == 0) ? acc[mt][nt][v] : red[idx] + acc[mt][nt][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kV6Threads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = red[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kV6Threads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kV6Warps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = (P.gmode == 3) ? p : P.gc * p;
+  for (int e = threadIdx.x; e < ne; e += kV6Threads) {
+    double sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = sum;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+template <int PM, int MTMAX>
+static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t st) {
+  constexpr int PM8 = PM < 8 ? 8 : PM;
+  constexpr int NT = PM8 / 8;
+  constexpr int kWarpWords = kRing6 * 8 * kSS6 + PM8 * kSS6;
+  auto k = tall_v6_kernel<PM, MTMAX>;
+  SlabPlan L;
+  L.nz = P.zin ? (P.p + 7) / 8 : 0;
+  L.n1 = (P.a1 + 7) / 8;
+  L.n2 = (P.a2 + 7) / 8;
+  L.ng = P.gmode == 1 ? (P.gc + 7) / 8 : 0;
+  L.total = L.nz + L.n1 + L.n2 + L.ng;
+  const int ks1 = (P.a1 + 3) / 4, ks2 = (P.a2 + 3) / 4;
+  const size_t smem = ((size_t)(ks1 + ks2) * NT * 32 + 2 * PM * PM + 2 + (size_t)kV6Warps * kWarpWords +
+                       (size_t)std::max(MTMAX * NT * 64, kV6Warps * PM)) * sizeof(double);
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kV6Threads, smem);
+    per_sm = v < 1 ? 1 : v;
+  }
+  const int64_t nunits = (P.n + 31) / 32;
+  int64_t g = (int64_t)sm_count() * per_sm;
+  if (g > max_grid) g = max_grid;
+  const int64_t need = (nunits + kV6Warps - 1) / kV6Warps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kV6Threads, smem, st>>>(P, L);
+  return cudaGetLastError();
+}
+
+#define RG_V6_CASE(PMv)                                                                   \
+  case PMv:                                                                               \
+    switch (mt5) {                                                                        \
+      case 0: e = launch_v6<PMv, 0>(P, bound, st); break;                                 \
+      case 2: e = launch_v6<PMv, 2>(P, bound, st); break;                                 \
+      case 6: e = launch_v6<PMv, 6>(P, bound, st); break;                                 \
+      case 12: e = launch_v6<PMv, 12>(P, bound, st); break;                               \
+      default: e = launch_v6<PMv, 16>(P, bound, st); break;                               \
+    }                                                                                     \
+    break;
+
 template <int PM, int MTMAX>
 static cudaError_t launch_v3(const TallParams& P, int64_t max_grid, cudaStream_t st) {
   constexpr int PM8 = PM < 8 ? 8 : PM;
@@ -983,10 +1361,31 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
       aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) && (gram_mode != 1 || aligned16(P.gb, P.ldgb)) ) {
     const char* impl = getenv("RG_TALL_IMPL");
     const int mt5 = (gram_mode == 1 || gram_mode == 2) ? mtmax : 0;
-    // v5 (cp.async Gram ring) wins for basis Grams, v3 for the rest
+    // default v6 (all operands through the cp.async ring, DMMA update);
+    // RG_TALL_IMPL=3 / 5 select the earlier variants for A/B runs
     // (tools/ab_tall.sh, profiles/ab_tall_r01.txt)
-    const bool use_v5 = impl ? impl[0] == '5' : gram_mode == 1;
-    if (!use_v5) {
+    // measured per pass type (profiles/ab_tall_r01.txt): v6 for passes with
+    // an update term or a triangular-solve store, v5 for a pure basis Gram,
+    // v3 for the self-Gram solve pass of CholQR2
+    int which = 6;
+    if (a1 + a2 == 0) {
+      if (gram_mode == 1)
+        which = 5;
+      else if (gram_mode == 2 && (d_r1 || d_r2))
+        which = 3;
+    }
+    if (impl) which = impl[0] - '0';
+    const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
+                           (gram_mode == 1 ? (gc + 7) / 8 : 0);
+    if (which == 6 && ncol_slabs <= kMaxSlabs) {
+      switch (PM) {
+        RG_V6_CASE(1)
+        RG_V6_CASE(2)
+        RG_V6_CASE(4)
+        RG_V6_CASE(8)
+        RG_V6_CASE(16)
+      }
+    } else if (which != 5) {
       switch (PM) {
         RG_V3_CASE(1)
         RG_V3_CASE(2)
