@@ -128,6 +128,33 @@ int rg_tsqr_f64(int64_t n, int32_t p, double* d_x, int64_t ldx, double* d_r,
                 void* d_work, int64_t work_bytes, void* stream);
 int64_t rg_tsqr_workspace_bytes(int64_t n, int32_t p);
 
+/*
+ * One CGS2 projection of an n x p block Z (in place) against C (n x k) and
+ * the basis W (n x w), in the reference's order (arnoldi.py:172-180: two
+ * passes, each C then W), as the fused rg_tall_f64 schedule the Python
+ * layer uses.  d_coef receives S1 (k x p) | c1 (w x p) | S2 | c2 packed
+ * column-major (F = S1 + S2, H = c1 + c2 on the host, arnoldi.py:177,180);
+ * if d_gram is non-NULL it receives Z^T Z of the projected block (the first
+ * CholQR Gram).  p <= 16, k + w <= 256.
+ */
+int rg_cgs2_f64(int64_t n, int32_t p, double* d_z, int64_t ldz,
+                const double* d_c, int64_t ldc, int32_t k,
+                const double* d_w, int64_t ldw, int32_t w,
+                double* d_coef, double* d_gram,
+                void* d_work, int64_t work_bytes, void* stream);
+
+/*
+ * CholQR2 of X (n x p, p <= 16) into Q (must not alias X): d_small holds
+ * G1 | R1 | G2 | R2 (4 p x p column-major blocks; R = R2 R1 with r_jj > 0),
+ * d_status[0..1] the two Cholesky statuses (non-zero: fall back to
+ * rg_tsqr_f64 on X, as reduced_qr does).  gram_ready != 0 means G1 = X^T X
+ * is already in d_small (e.g. from rg_cgs2_f64's d_gram).
+ * Replaces np.linalg.qr in reduced_qr (dense_kernels.py:41).
+ */
+int rg_cholqr2_f64(int64_t n, int32_t p, const double* d_x, int64_t ldx, double* d_q, int64_t ldq,
+                   double* d_small, int32_t* d_status, int32_t gram_ready,
+                   void* d_work, int64_t work_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

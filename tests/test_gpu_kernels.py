@@ -269,3 +269,44 @@ def test_reduced_qr_wide_blocks(cuda, L):
     assert _rel(f.r_factor, r_ref) <= 1e-12 * np.linalg.cond(X)
     assert np.linalg.norm(f.q.T @ f.q - np.eye(L)) <= 1e-13 * L
     assert np.abs(f.q - q_ref).max() <= 1e-11
+
+
+def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
+    """The orchestration entry points a non-Python host would call
+    (include/rgb200.h: rg_cgs2_f64, rg_cholqr2_f64) reproduce the oracle's
+    CGS2 (arnoldi.py:172-180) and thin QR."""
+    from paper_1604_01713_b200 import _lib
+    from paper_1604_01713_b200 import device as D
+
+    L = _lib.load()
+    rng = np.random.default_rng(21)
+    n, p, k, w = 50_000, 8, 20, 40
+    C = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    W = np.linalg.qr(rng.standard_normal((n, w)))[0]
+    A = rng.standard_normal((n, p))
+    ref, F, H = oracle.cgs2_project(A, C, W)
+    Zd, Cd, Wd = D.to_device_block(A), D.to_device_block(C), D.to_device_block(W)
+    coef = torch.zeros((2 * k + 2 * w) * p, dtype=torch.float64, device=cuda)
+    small = torch.zeros(4 * p * p, dtype=torch.float64, device=cuda)
+    ws = D.Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k, w)))
+    rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), Cd.data_ptr(), D.ld_of(Cd), k, Wd.data_ptr(), D.ld_of(Wd), w,
+                       coef.data_ptr(), small.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+    assert rc == 0
+    hc = coef.cpu().numpy()
+    S1 = hc[:k * p].reshape(p, k).T
+    c1 = hc[k * p:(k + w) * p].reshape(p, w).T
+    S2 = hc[(k + w) * p:(2 * k + w) * p].reshape(p, k).T
+    c2 = hc[(2 * k + w) * p:].reshape(p, w).T
+    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12 * 1e3
+    assert np.abs(S1 + S2 - F).max() <= 1e-12 * np.abs(F).max() * 10
+    assert np.abs(c1 + c2 - H).max() <= 1e-12 * np.abs(H).max() * 10
+    Qd = D.empty_block(n, p)
+    status = torch.zeros(2, dtype=torch.int32, device=cuda)
+    rc = L.rg_cholqr2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), Qd.data_ptr(), D.ld_of(Qd), small.data_ptr(),
+                          status.data_ptr(), 1, ws.data_ptr(), ws.numel(), D.stream_ptr())
+    assert rc == 0 and status.cpu().tolist() == [0, 0]
+    sm = small.cpu().numpy().reshape(4, p, p).transpose(0, 2, 1)
+    R = np.triu(sm[3] @ sm[1])
+    q_ref, r_ref, _ = oracle.reduced_qr(ref)
+    assert _rel(R, r_ref) <= 1e-11
+    assert np.abs(D.to_numpy_block(Qd) - q_ref).max() <= 1e-10
