@@ -242,12 +242,16 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     Vnew = fact.v_block(m + 1)
 
     if ortho == "cgs2":
-        S1, c1, S2, c2 = fact._coef_views(m)
-        if C is not None:
-            bases, coefs = [C, active, C, active], [S1, c1, S2, c2]
+        if _dev.fused_ok() and L <= _dev.MAX_P and fact.k + (m + 1) * L <= 256:
+            # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64)
+            _dev.cgs2(Ahat, C, active, fact._coef, scr.G1)
         else:
-            bases, coefs = [active, active], [c1, c2]
-        project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.MAX_P else None)
+            S1, c1, S2, c2 = fact._coef_views(m)
+            if C is not None:
+                bases, coefs = [C, active, C, active], [S1, c1, S2, c2]
+            else:
+                bases, coefs = [active, active], [c1, c2]
+            project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.MAX_P else None)
         ncoef = (2 * fact.k + 2 * (m + 1) * L) * L
         fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
         R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.MAX_P)

@@ -93,6 +93,10 @@ def cholqr2_launch(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch, g1_ready: b
     """Enqueue CholQR2 of X into Q (Q may not alias X: X is kept intact for
     the TSQR fallback).  If ``g1_ready``, scr.G1 already holds X^T X (fused
     into the producing pass)."""
+    if _dev.fused_ok() and X.shape[1] <= _dev.MAX_P:
+        # G1 | R1 | G2 | R2 are the first four blocks of scr.buf, as rg_cholqr2_f64 expects
+        _dev.cholqr2(X, Q, scr.buf, scr.status, g1_ready)
+        return
     if not g1_ready:
         _dev.tall(X, None, gram=("self", scr.G1))
     _dev.chol(scr.G1, scr.R1, scr.status[0:1], CHOL_COND_TOL)

@@ -431,6 +431,37 @@ def _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx):
             tall(zc, None, gram=("sumsq", gram[1][c0:c1]), n=n, p=c1 - c0)
 
 
+def fused_ok() -> bool:
+    """The C orchestrators (rg_cgs2_f64 / rg_cholqr2_f64) replace the Python
+    pass chain on one GPU; row-partitioned runs need the Gram allreduce
+    between passes, and bench attribution times each launch."""
+    return _COMM is None and not LaunchLog.timing
+
+
+def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1) -> None:
+    """One call: CGS2 of Z against C then W (twice) in place; coef receives
+    S1|c1|S2|c2; G1 (optional) receives Z^T Z of the result."""
+    L = lib()
+    n, p = Z.shape
+    k = 0 if C is None else C.shape[1]
+    w = W.shape[1]
+    ws = Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k, w, p)))
+    rc = L.rg_cgs2_f64(n, p, Z.data_ptr(), ld_of(Z), ptr(C), ld_of(C) if C is not None else 1, k,
+                       W.data_ptr(), ld_of(W), w, coef.data_ptr(), ptr(G1), ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check(rc, "cgs2")
+    LaunchLog.count += (2 if k else 0) + (2 if w else 0) + 1
+
+
+def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch.Tensor, gram_ready: bool) -> None:
+    L = lib()
+    n, p = X.shape
+    ws = Workspace.get(L.rg_tall_workspace_bytes(n, p, 0, 0, 2, p))
+    rc = L.rg_cholqr2_f64(n, p, X.data_ptr(), ld_of(X), Q.data_ptr(), ld_of(Q), small.data_ptr(), status.data_ptr(),
+                          1 if gram_ready else 0, ws.data_ptr(), ws.numel(), stream_ptr())
+    _lib.check(rc, "cholqr2")
+    LaunchLog.count += 4 + (0 if gram_ready else 1)
+
+
 def chol(G: torch.Tensor, R: torch.Tensor, status: torch.Tensor, cond_tol: float):
     p = G.shape[0]
     e0 = _t0()
