@@ -155,6 +155,29 @@ int rg_cholqr2_f64(int64_t n, int32_t p, const double* d_x, int64_t ldx, double*
                    double* d_small, int32_t* d_status, int32_t gram_ready,
                    void* d_work, int64_t work_bytes, void* stream);
 
+/*
+ * complex128 twins (BASELINE configs[4]; the reference is real-only, so these
+ * follow the complex restatement of SURVEY.md §8c: conjugate transposes,
+ * real non-negative r_jj).  Complex blocks are column-major arrays of
+ * interleaved (re, im) doubles; ld counts complex elements.
+ *   rg_spmm_csr_c128  as rg_spmm_csr_f64 (vals interleaved complex); every
+ *                     partial product and sum of (a*x) is rounded separately
+ *   rg_tall_c128      as rg_tall_f64 with Gout = Gb^H z / z^H z, p <= 8,
+ *                     gc <= 48, mode 3 writes p real sums of |z|^2
+ *   rg_chol_c128      Hermitian Cholesky G = R^H R, p <= 64
+ */
+int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_end,
+                     const int32_t* d_row_ptr, const int32_t* d_col_idx, const double* d_vals,
+                     const double* d_x, int64_t ldx, int64_t n_local, const double* d_xg, int64_t ldg,
+                     int32_t p, double* d_y, int64_t ldy, void* stream);
+int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t ldzin, double* d_zout, int64_t ldzout,
+                 const double* d_x1, int64_t ldx1, int32_t a1, const double* d_s1, double alpha1,
+                 const double* d_x2, int64_t ldx2, int32_t a2, const double* d_s2, double alpha2,
+                 const double* d_r1, const double* d_r2, int32_t gram_mode, const double* d_gb, int64_t ldgb,
+                 int32_t gc, double* d_gout, void* d_work, int64_t work_bytes, void* stream);
+int64_t rg_tall_c128_workspace_bytes(int64_t n, int32_t p, int32_t a1, int32_t a2, int32_t gram_mode, int32_t gc);
+int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, double cond_tol, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,605 @@
+// Complex128 twins of the hot-path kernels (BASELINE configs[4]: 27-point
+// complex stencil, shifted-Helmholtz-like).  The reference is real-only
+// (sparse_core.py:53 truncates complex input), so these kernels follow the
+// complex restatement of SURVEY.md §8c: transposes become conjugate
+// transposes and the r_jj >= 0 convention becomes r_jj real >= 0.
+//
+//   rg_spmm_csr_c128  persistent CSR x block; each complex multiply-add is
+//                     (ar*xr - ai*xi, ar*xi + ai*xr) with every product and
+//                     sum separately rounded, in ascending storage order --
+//                     bitwise equal to oracle/spmm_oracle.c:oracle_spmm_c128
+//   rg_tall_c128      lane-per-row complex update / triangular solves on the
+//                     CUDA cores; Gram Gb^H z on DMMA m8n8k4 with four real
+//                     products per complex tile (Cr += Ar Br + Ai Bi,
+//                     Ci += Ar Bi - Ai Br), Gb staged through warp-private
+//                     smem slabs (real and imaginary planes)
+//   rg_chol_c128      Hermitian Cholesky G = R^H R, real positive diagonal
+//
+// Complex blocks are column-major arrays of interleaved (re, im) doubles.
+#include "rg_common.cuh"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace rg {
+
+__device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// ----------------------------------------------------------------------------
+// SpMM
+// ----------------------------------------------------------------------------
+
+constexpr int kCWarps = 8;
+constexpr int kCChunk = 256;
+
+template <int PB, bool GHOST>
+__global__ void __launch_bounds__(kCWarps * 32, 2)
+spmm_c128_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
+                 const int32_t* __restrict__ ci, const double2* __restrict__ va,
+                 const double2* __restrict__ X, int64_t ldx, int64_t n_local,
+                 const double2* __restrict__ Xg, int64_t ldg, double2* __restrict__ Y, int64_t ldy) {
+  __shared__ int32_t s_ci[kCWarps][kCChunk];
+  __shared__ double2 s_va[kCWarps][kCChunk];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t nunits = (row_end - row_begin + 31) / 32;
+  const int64_t nwarps = (int64_t)gridDim.x * kCWarps;
+  for (int64_t u = (int64_t)blockIdx.x * kCWarps + w; u < nunits; u += nwarps) {
+    const int64_t wrow0 = row_begin + u * 32;
+    const int64_t wlast = min(wrow0 + 32, row_end);
+    const int64_t i = wrow0 + lane;
+    const bool valid = i < row_end;
+    const int32_t wbeg = __ldg(rp + wrow0), wend = __ldg(rp + wlast);
+    const int32_t mybeg = valid ? __ldg(rp + i) : 0, myend = valid ? __ldg(rp + i + 1) : 0;
+    double ar_[PB], ai_[PB];
+#pragma unroll
+    for (int c = 0; c < PB; ++c) ar_[c] = ai_[c] = 0.0;
+    for (int32_t base = wbeg; base < wend; base += kCChunk) {
+      const int32_t cnt = min(kCChunk, wend - base);
+      __syncwarp();
+      for (int e = lane; e < cnt; e += 32) {
+        s_ci[w][e] = __ldg(ci + base + e);
+        s_va[w][e] = __ldg(va + base + e);
+      }
+      __syncwarp();
+      const int lo = max(mybeg, base) - base, hi = min(myend, base + cnt) - base;
+      double2 xn[PB];
+      double2 an = make_double2(0.0, 0.0);
+      auto gather = [&](int t, double2 (&xv)[PB]) {
+        const int64_t j = s_ci[w][t];
+        const double2* xp = X + j;
+        int64_t ld = ldx;
+        if (GHOST && j >= n_local) {
+          xp = Xg + (j - n_local);
+          ld = ldg;
+        }
+#pragma unroll
+        for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
+      };
+      if (lo < hi) {
+        an = s_va[w][lo];
+        gather(lo, xn);
+      }
+      for (int t = lo; t < hi; ++t) {
+        double2 xc[PB];
+#pragma unroll
+        for (int c = 0; c < PB; ++c) xc[c] = xn[c];
+        const double2 a = an;
+        if (t + 1 < hi) {
+          an = s_va[w][t + 1];
+          gather(t + 1, xn);
+        }
+#pragma unroll
+        for (int c = 0; c < PB; ++c) {
+          const double pr = __dsub_rn(__dmul_rn(a.x, xc[c].x), __dmul_rn(a.y, xc[c].y));
+          const double pi = __dadd_rn(__dmul_rn(a.x, xc[c].y), __dmul_rn(a.y, xc[c].x));
+          ar_[c] = __dadd_rn(ar_[c], pr);
+          ai_[c] = __dadd_rn(ai_[c], pi);
+        }
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < PB; ++c) Y[i + c * ldy] = make_double2(ar_[c], ai_[c]);
+    }
+  }
+}
+
+template <int PB>
+static void launch_spmm_c(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double2* va,
+                          const double2* X, int64_t ldx, int64_t n_local, const double2* Xg, int64_t ldg, double2* Y,
+                          int64_t ldy, cudaStream_t s) {
+  const int64_t units = (re - rb + 31) / 32;
+  int64_t g = (int64_t)sm_count() * 2;
+  const int64_t need = (units + kCWarps - 1) / kCWarps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  if (Xg)
+    spmm_c128_kernel<PB, true><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg, Y,
+                                                                     ldy);
+  else
+    spmm_c128_kernel<PB, false><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg,
+                                                                      Y, ldy);
+}
+
+// ----------------------------------------------------------------------------
+// tall-skinny complex passes
+// ----------------------------------------------------------------------------
+
+struct TallC {
+  int64_t n;
+  int p;
+  const double2* zin;
+  int64_t ldzin;
+  double2* zout;
+  int64_t ldzout;
+  const double2* x1;
+  int64_t ldx1;
+  int a1;
+  const double2* s1;
+  double alpha1;
+  const double2* x2;
+  int64_t ldx2;
+  int a2;
+  const double2* s2;
+  double alpha2;
+  const double2* r1;
+  const double2* r2;
+  int gmode;
+  const double2* gb;
+  int64_t ldgb;
+  int gc;
+  int mtiles;
+  double2* gout;   // modes 1/2: gc x p complex; mode 3: p doubles (as double2 storage reused)
+  double* part;
+  unsigned* counter;
+};
+
+constexpr int kTCWarps = 8;
+constexpr int kTCThreads = kTCWarps * 32;
+constexpr int kCS = 36;  // slab stride
+
+template <int PM>
+__device__ __forceinline__ void capply(double (&zr)[PM], double (&zi)[PM], const double2* __restrict__ X, int64_t ldx,
+                                       int a, const double2* sS, double alpha, int64_t i) {
+  double mr[PM], mi[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) mr[c] = mi[c] = 0.0;
+  for (int a0 = 0; a0 < a; a0 += 4) {
+    double2 xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xv[u] = a0 + u < a ? __ldg(X + i + (int64_t)(a0 + u) * ldx) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (a0 + u < a) {
+        const double2* srow = sS + (a0 + u) * PM;
+#pragma unroll
+        for (int c = 0; c < PM; ++c) {
+          const double2 s = srow[c];
+          mr[c] = fma(xv[u].x, s.x, mr[c]);
+          mr[c] = fma(-xv[u].y, s.y, mr[c]);
+          mi[c] = fma(xv[u].x, s.y, mi[c]);
+          mi[c] = fma(xv[u].y, s.x, mi[c]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < PM; ++c) {
+    zr[c] = zr[c] + alpha * mr[c];
+    zi[c] = zi[c] + alpha * mi[c];
+  }
+}
+
+// y R = z, R upper triangular complex with real diagonal; sR row-major, the
+// diagonal slot holds 1 / r_jj (real part)
+template <int PM>
+__device__ __forceinline__ void ctrsm(double (&zr)[PM], double (&zi)[PM], const double2* sR, int p) {
+#pragma unroll
+  for (int j = 0; j < PM; ++j) {
+    if (j < p) {
+      double yr = zr[j], yi = zi[j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) {
+        const double2 r = sR[k * PM + j];
+        yr = fma(-zr[k], r.x, yr);
+        yr = fma(zi[k], r.y, yr);
+        yi = fma(-zr[k], r.y, yi);
+        yi = fma(-zi[k], r.x, yi);
+      }
+      const double inv = sR[j * PM + j].x;
+      zr[j] = yr * inv;
+      zi[j] = yi * inv;
+    }
+  }
+}
+
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kTCThreads, 1) tall_c128_kernel(TallC P) {
+  extern __shared__ __align__(16) double smem[];
+  const int p = P.p;
+  double2* sS1 = reinterpret_cast<double2*>(smem);  // [a1][PM]
+  double2* sS2 = sS1 + P.a1 * PM;
+  double2* sR1 = sS2 + P.a2 * PM;                  // PM x PM row-major
+  double2* sR2 = sR1 + PM * PM;
+  double* wb = reinterpret_cast<double*>(sR2 + PM * PM);
+  // per warp: z tile re/im [8][kCS] each, Gb slab re/im [8][kCS] each
+  constexpr int kWarpWords = 4 * 8 * kCS;
+  double* red = wb + kTCWarps * kWarpWords;
+
+  for (int e = threadIdx.x; e < P.a1 * PM; e += kTCThreads) {
+    const int aa = e / PM, c = e % PM;
+    sS1[e] = c < p ? P.s1[aa + (int64_t)c * P.a1] : make_double2(0.0, 0.0);
+  }
+  for (int e = threadIdx.x; e < P.a2 * PM; e += kTCThreads) {
+    const int aa = e / PM, c = e % PM;
+    sS2[e] = c < p ? P.s2[aa + (int64_t)c * P.a2] : make_double2(0.0, 0.0);
+  }
+  for (int e = threadIdx.x; e < PM * PM; e += kTCThreads) {
+    const int ii = e / PM, jj = e % PM;
+    const double2 id = make_double2(ii == jj ? 1.0 : 0.0, 0.0);
+    double2 v1 = id, v2 = id;
+    if (P.r1 && ii < p && jj < p) {
+      v1 = P.r1[ii + (int64_t)jj * p];
+      if (ii == jj) v1 = make_double2(1.0 / v1.x, 0.0);
+    }
+    if (P.r2 && ii < p && jj < p) {
+      v2 = P.r2[ii + (int64_t)jj * p];
+      if (ii == jj) v2 = make_double2(1.0 / v2.x, 0.0);
+    }
+    sR1[e] = v1;
+    sR2[e] = v2;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  double* ztr = wb + warp * kWarpWords;
+  double* zti = ztr + 8 * kCS;
+  double* gsr = zti + 8 * kCS;
+  double* gsi = gsr + 8 * kCS;
+  const bool gram = P.gmode == 1 || P.gmode == 2;
+  const int mtiles = P.mtiles;
+  double acc[MTMAX][2][2];  // [tile][re/im][c-fragment]
+#pragma unroll
+  for (int mt = 0; mt < MTMAX; ++mt) acc[mt][0][0] = acc[mt][0][1] = acc[mt][1][0] = acc[mt][1][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  const int64_t nunits = (P.n + 31) / 32;
+  const int64_t gwarp = (int64_t)blockIdx.x * kTCWarps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kTCWarps;
+  for (int64_t u = gwarp; u < nunits; u += nwarps) {
+    const int64_t r0 = u * 32;
+    const int64_t i = r0 + lane;
+    const bool valid = i < P.n;
+    double zr[PM], zi[PM];
+#pragma unroll
+    for (int c = 0; c < PM; ++c) zr[c] = zi[c] = 0.0;
+    if (valid) {
+      if (P.zin) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) {
+            const double2 v = __ldg(P.zin + i + (int64_t)c * P.ldzin);
+            zr[c] = v.x;
+            zi[c] = v.y;
+          }
+      }
+      if (P.a1) capply<PM>(zr, zi, P.x1, P.ldx1, P.a1, sS1, P.alpha1, i);
+      if (P.a2) capply<PM>(zr, zi, P.x2, P.ldx2, P.a2, sS2, P.alpha2, i);
+      if (P.r1) ctrsm<PM>(zr, zi, sR1, p);
+      if (P.r2) ctrsm<PM>(zr, zi, sR2, p);
+      if (P.zout) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) P.zout[i + (int64_t)c * P.ldzout] = make_double2(zr[c], zi[c]);
+      }
+      if (P.gmode == 3) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) sq[c] = fma(zr[c], zr[c], fma(zi[c], zi[c], sq[c]));
+      }
+    }
+    if (!gram) continue;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      ztr[c * kCS + lane] = c < PM ? zr[c < PM ? c : 0] : 0.0;
+      zti[c * kCS + lane] = c < PM ? zi[c < PM ? c : 0] : 0.0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int mt = 0; mt < MTMAX; ++mt) {
+      if (mt < mtiles) {
+        const double* ar_ = ztr;
+        const double* ai_ = zti;
+        if (P.gmode == 1) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int gg = mt * 8 + c;
+            const double2 v = (valid && gg < P.gc) ? __ldg(P.gb + i + (int64_t)gg * P.ldgb) : make_double2(0.0, 0.0);
+            gsr[c * kCS + lane] = v.x;
+            gsi[c * kCS + lane] = v.y;
+          }
+          __syncwarp();
+          ar_ = gsr;
+          ai_ = gsi;
+        }
+        const int cb = P.gmode == 1 ? 0 : mt * 8;  // self Gram: A = z tile rows mt*8.. (PM <= 8 -> mt == 0)
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const double a_r = ar_[(cb + mrow) * kCS + ks * 4 + kq];
+          const double a_i = ai_[(cb + mrow) * kCS + ks * 4 + kq];
+          const double b_r = ztr[mrow * kCS + ks * 4 + kq];
+          const double b_i = zti[mrow * kCS + ks * 4 + kq];
+          dmma_c(acc[mt][0][0], acc[mt][0][1], a_r, b_r);
+          dmma_c(acc[mt][0][0], acc[mt][0][1], a_i, b_i);
+          dmma_c(acc[mt][1][0], acc[mt][1][1], a_r, b_i);
+          dmma_c(acc[mt][1][0], acc[mt][1][1], -a_i, b_r);
+        }
+        __syncwarp();
+      }
+    }
+  }
+
+  __shared__ bool s_last;
+  __syncthreads();
+  if (gram) {
+    for (int ww = 0; ww < kTCWarps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTMAX; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * 2 + ri) * 32 + lane) * 2 + v;
+                red[idx] = (ww == 0) ? acc[mt][ri][v] : red[idx] + acc[mt][ri][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kTCThreads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7;
+      const int ln = mr * 4 + (c >> 1), v = c & 1;
+      P.part[((int64_t)blockIdx.x * ne + e) * 2] = red[((mt * 2 + 0) * 32 + ln) * 2 + v];
+      P.part[((int64_t)blockIdx.x * ne + e) * 2 + 1] = red[((mt * 2 + 1) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kTCThreads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kTCWarps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (P.gmode == 3) {
+    double* out = reinterpret_cast<double*>(P.gout);
+    for (int e = threadIdx.x; e < p; e += kTCThreads) {
+      double sum = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * p + e);
+      out[e] = sum;
+    }
+  } else {
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kTCThreads) {
+      double sr = 0.0, si = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        sr += __ldcg(P.part + ((int64_t)b * ne + e) * 2);
+        si += __ldcg(P.part + ((int64_t)b * ne + e) * 2 + 1);
+      }
+      P.gout[e] = make_double2(sr, si);
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+template <int PM, int MTMAX>
+static cudaError_t launch_tall_c(const TallC& P, cudaStream_t st) {
+  auto k = tall_c128_kernel<PM, MTMAX>;
+  const size_t smem = ((size_t)(P.a1 + P.a2) * PM * 2 + 4 * PM * PM + (size_t)kTCWarps * 4 * 8 * kCS +
+                       (size_t)std::max(MTMAX * 2 * 64, kTCWarps * PM)) * sizeof(double);
+  static bool cfg = false;
+  if (!cfg) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cfg = true;
+  }
+  const int64_t nunits = (P.n + 31) / 32;
+  int64_t g = (int64_t)sm_count();
+  const int64_t need = (nunits + kTCWarps - 1) / kTCWarps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kTCThreads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------------------
+// Hermitian Cholesky
+// ----------------------------------------------------------------------------
+
+__global__ void chol_c128_kernel(int p, const double2* __restrict__ G, double2* __restrict__ R, int* status,
+                                 double cond_tol) {
+  extern __shared__ double2 sA[];
+  __shared__ int s_bad;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) sA[e] = G[e];
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int j = 0; j < p; ++j) gmax = fmax(gmax, sA[j + j * p].x);
+  for (int j = 0; j < p; ++j) {
+    if (threadIdx.x == 0) {
+      double d = sA[j + j * p].x;
+      for (int k = 0; k < j; ++k) {
+        const double2 r = sA[k + j * p];
+        d -= r.x * r.x + r.y * r.y;
+      }
+      if (!(d > 0.0) || !isfinite(d)) {
+        s_bad = 1;
+        d = 1.0;
+      }
+      sA[j + j * p] = make_double2(sqrt(d), 0.0);
+    }
+    __syncthreads();
+    const double rjj = sA[j + j * p].x;
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) {
+      // R[j][i] = (G[j][i] - sum_k conj(R[k][j]) R[k][i]) / r_jj
+      double vr = sA[j + i * p].x, vi = sA[j + i * p].y;
+      for (int k = 0; k < j; ++k) {
+        const double2 a = sA[k + j * p], b = sA[k + i * p];
+        vr -= a.x * b.x + a.y * b.y;
+        vi -= a.x * b.y - a.y * b.x;
+      }
+      sA[j + i * p] = make_double2(vr / rjj, vi / rjj);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int st = s_bad;
+    if (!st) {
+      double dmin = sA[0].x;
+      for (int j = 1; j < p; ++j) dmin = fmin(dmin, sA[j + j * p].x);
+      if (dmin * dmin < cond_tol * gmax) st = 2;
+    }
+    *status = st;
+  }
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int r = e % p, c = e / p;
+    R[e] = r <= c ? sA[e] : make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace rg
+
+extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_row_ptr,
+                                const int32_t* d_col_idx, const double* d_vals, const double* d_x, int64_t ldx,
+                                int64_t n_local, const double* d_xg, int64_t ldg, int32_t p, double* d_y,
+                                int64_t ldy, void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n_rows >= 0 && 0 <= row_begin && row_begin <= row_end && row_end <= n_rows,
+             "rg_spmm_csr_c128: bad row range");
+  RG_REQUIRE(p >= 1 && d_row_ptr && d_y && ldy >= n_rows, "rg_spmm_csr_c128: bad arguments");
+  if (row_end == row_begin) return RG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double2* X = reinterpret_cast<const double2*>(d_x);
+  const double2* Xg = reinterpret_cast<const double2*>(d_xg);
+  double2* Y = reinterpret_cast<double2*>(d_y);
+  const double2* va = reinterpret_cast<const double2*>(d_vals);
+  for (int c0 = 0; c0 < p;) {
+    const int rem = p - c0;
+    const int pc = rem >= 8 ? 8 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
+    const double2* Xc = X ? X + (int64_t)c0 * ldx : nullptr;
+    const double2* Xgc = Xg ? Xg + (int64_t)c0 * ldg : nullptr;
+    double2* Yc = Y + (int64_t)c0 * ldy;
+    switch (pc) {
+      case 1: launch_spmm_c<1>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
+      case 2: launch_spmm_c<2>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
+      case 4: launch_spmm_c<4>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
+      default: launch_spmm_c<8>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
+    }
+    RG_CHECK_LAUNCH("rg_spmm_csr_c128");
+    c0 += pc;
+  }
+  return RG_OK;
+}
+
+extern "C" int64_t rg_tall_c128_workspace_bytes(int64_t n, int32_t p, int32_t a1, int32_t a2, int32_t gram_mode,
+                                                int32_t gc) {
+  (void)n; (void)a1; (void)a2;
+  int64_t ne = 0;
+  if (gram_mode == 1) ne = (int64_t)gc * p * 2;
+  if (gram_mode == 2) ne = (int64_t)p * p * 2;
+  if (gram_mode == 3) ne = p;
+  return 256 + (int64_t)rg::sm_count() * ne * (int64_t)sizeof(double);
+}
+
+extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t ldzin, double* d_zout, int64_t ldzout,
+                            const double* d_x1, int64_t ldx1, int32_t a1, const double* d_s1, double alpha1,
+                            const double* d_x2, int64_t ldx2, int32_t a2, const double* d_s2, double alpha2,
+                            const double* d_r1, const double* d_r2, int32_t gram_mode, const double* d_gb,
+                            int64_t ldgb, int32_t gc, double* d_gout, void* d_work, int64_t work_bytes,
+                            void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n >= 0 && p >= 1 && p <= 8, "rg_tall_c128: p=%d outside [1, 8]", p);
+  RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= 256, "rg_tall_c128: term widths %d, %d", a1, a2);
+  RG_REQUIRE(a1 == 0 || (d_x1 && d_s1 && ldx1 >= n), "rg_tall_c128: bad term 1");
+  RG_REQUIRE(a2 == 0 || (d_x2 && d_s2 && ldx2 >= n), "rg_tall_c128: bad term 2");
+  RG_REQUIRE(gram_mode >= 0 && gram_mode <= 3, "rg_tall_c128: gram_mode %d", gram_mode);
+  RG_REQUIRE(gram_mode != 1 || (d_gb && gc >= 1 && gc <= 48 && ldgb >= n),
+             "rg_tall_c128: Gram basis width gc=%d outside [1, 48]", gc);
+  RG_REQUIRE(gram_mode != 2 || gc == p, "rg_tall_c128: self Gram needs gc == p");
+  RG_REQUIRE(gram_mode == 0 || d_gout, "rg_tall_c128: null Gram output");
+  if (gram_mode == 3) gc = 1;
+  const int64_t need = rg_tall_c128_workspace_bytes(n, p, a1, a2, gram_mode, gc);
+  RG_REQUIRE(gram_mode == 0 || (d_work && work_bytes >= need), "rg_tall_c128: workspace too small");
+  TallC P;
+  P.n = n; P.p = p;
+  P.zin = reinterpret_cast<const double2*>(d_zin); P.ldzin = ldzin;
+  P.zout = reinterpret_cast<double2*>(d_zout); P.ldzout = ldzout;
+  P.x1 = reinterpret_cast<const double2*>(d_x1); P.ldx1 = ldx1; P.a1 = a1;
+  P.s1 = reinterpret_cast<const double2*>(d_s1); P.alpha1 = alpha1;
+  P.x2 = reinterpret_cast<const double2*>(d_x2); P.ldx2 = ldx2; P.a2 = a2;
+  P.s2 = reinterpret_cast<const double2*>(d_s2); P.alpha2 = alpha2;
+  P.r1 = reinterpret_cast<const double2*>(d_r1); P.r2 = reinterpret_cast<const double2*>(d_r2);
+  P.gmode = gram_mode; P.gb = reinterpret_cast<const double2*>(d_gb); P.ldgb = ldgb; P.gc = gc;
+  P.mtiles = (gram_mode == 1 || gram_mode == 2) ? (gc + 7) / 8 : 0;
+  P.gout = reinterpret_cast<double2*>(d_gout);
+  P.counter = (unsigned*)d_work;
+  P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
+  if (gram_mode == 0 && n == 0) return RG_OK;
+  const int PM = p <= 1 ? 1 : (p <= 2 ? 2 : (p <= 4 ? 4 : 8));
+  const int mtmax = P.mtiles <= 2 ? 2 : 6;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+#define RG_TC(PMv)                                                          \
+  case PMv:                                                                 \
+    e = mtmax == 2 ? launch_tall_c<PMv, 2>(P, st) : launch_tall_c<PMv, 6>(P, st); \
+    break;
+  switch (PM) {
+    RG_TC(1)
+    RG_TC(2)
+    RG_TC(4)
+    default: e = mtmax == 2 ? launch_tall_c<8, 2>(P, st) : launch_tall_c<8, 6>(P, st); break;
+  }
+#undef RG_TC
+  if (e != cudaSuccess) {
+    set_error("rg_tall_c128: %s", cudaGetErrorString(e));
+    return RG_ECUDA;
+  }
+  return RG_OK;
+}
+
+extern "C" int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, double cond_tol,
+                            void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(p >= 1 && p <= 64 && d_g && d_r && d_status, "rg_chol_c128: bad arguments");
+  chol_c128_kernel<<<1, 64, (size_t)p * p * sizeof(double2), (cudaStream_t)stream>>>(
+      p, reinterpret_cast<const double2*>(d_g), reinterpret_cast<double2*>(d_r), d_status, cond_tol);
+  RG_CHECK_LAUNCH("rg_chol_c128");
+  return RG_OK;
+}

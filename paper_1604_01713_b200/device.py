@@ -21,6 +21,9 @@ LD_ALIGN = 32
 MAX_P = 16        # block width one rg_tall launch handles
 MAX_GC = 128      # Gram basis columns per launch
 MAX_TERM_COLS = 512
+MAX_P_C = 8       # complex128 limits (rg_tall_c128)
+MAX_GC_C = 48
+MAX_TERM_COLS_C = 256
 
 
 _COMM = None   # distributed.CommContext when row-partitioned (Gram allreduce)
@@ -130,6 +133,8 @@ def to_device_block(x, device=None, dtype=torch.float64) -> torch.Tensor:
     a = np.asarray(x)
     if a.ndim == 1:
         a = a.reshape(-1, 1)
+    if np.iscomplexobj(a):
+        dtype = torch.complex128
     np_dtype = np.complex128 if dtype == torch.complex128 else np.float64
     a = np.asfortranarray(a, dtype=np_dtype)
     out = empty_block(a.shape[0], a.shape[1], dev, dtype)
@@ -310,15 +315,16 @@ def _coef(S: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def _split_terms(terms):
-    """Split wide terms so that each launch stages <= MAX_TERM_COLS columns."""
+def _split_terms(terms, max_cols=None):
+    """Split wide terms so that each launch stages <= max_cols columns."""
+    max_cols = MAX_TERM_COLS if max_cols is None else max_cols
     pieces = []
     for X, S, alpha in terms:
         a = X.shape[1]
         if a == 0:
             continue
-        for a0 in range(0, a, MAX_TERM_COLS):
-            a1 = min(a, a0 + MAX_TERM_COLS)
+        for a0 in range(0, a, max_cols):
+            a1 = min(a, a0 + max_cols)
             pieces.append((X[:, a0:a1], _coef(S[a0:a1, :]), alpha))
     return pieces
 
@@ -339,10 +345,11 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         _zero_gram(gram)
         return
     cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
-    terms = _split_terms(terms)
+    maxp, maxgc = (MAX_P_C, MAX_GC_C) if cplx else (MAX_P, MAX_GC)
+    terms = _split_terms(terms, MAX_TERM_COLS_C if cplx else MAX_TERM_COLS)
     r1 = _coef(r1) if r1 is not None else None
     r2 = _coef(r2) if r2 is not None else None
-    if p > MAX_P:
+    if p > maxp:
         _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx)
         return
     gmode, gb, gout = 0, None, None
@@ -357,17 +364,18 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         else:
             raise ValueError(f"unknown gram kind {kind!r}")
     # passes over the term list (<= 2 terms and <= MAX_TERM_COLS staged columns each)
+    tcols = MAX_TERM_COLS_C if cplx else MAX_TERM_COLS
     groups, cur_g, cur_cols = [], [], 0
     for t in terms:
         a = t[0].shape[1]
-        if cur_g and (len(cur_g) == 2 or cur_cols + a > MAX_TERM_COLS):
+        if cur_g and (len(cur_g) == 2 or cur_cols + a > tcols):
             groups.append(cur_g)
             cur_g, cur_cols = [], 0
         cur_g.append(t)
         cur_cols += a
     if cur_g or not groups:
         groups.append(cur_g)
-    needs_multi = len(groups) > 1 or (gmode == 1 and gb.shape[1] > MAX_GC)
+    needs_multi = len(groups) > 1 or (gmode == 1 and gb.shape[1] > maxgc)
     zbuf = Z_out
     if needs_multi and zbuf is None:
         zbuf = empty_block(n, p, Z_in.device if Z_in is not None else None,
@@ -381,11 +389,11 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
             _tall_call(n, p, cur_in, zbuf, t1, t2, None, None, 0, None, None, cplx)
             cur_in = zbuf
             continue
-        if gmode == 1 and gb.shape[1] > MAX_GC:
+        if gmode == 1 and gb.shape[1] > maxgc:
             gc = gb.shape[1]
-            _tall_call(n, p, cur_in, zbuf, t1, t2, r1, r2, 1, gb[:, :MAX_GC], gout[:MAX_GC, :], cplx)
-            for g0 in range(MAX_GC, gc, MAX_GC):
-                g1 = min(gc, g0 + MAX_GC)
+            _tall_call(n, p, cur_in, zbuf, t1, t2, r1, r2, 1, gb[:, :maxgc], gout[:maxgc, :], cplx)
+            for g0 in range(maxgc, gc, maxgc):
+                g1 = min(gc, g0 + maxgc)
                 _tall_call(n, p, zbuf, None, None, None, None, None, 1, gb[:, g0:g1], gout[g0:g1, :], cplx)
         else:
             _tall_call(n, p, cur_in, zbuf if needs_multi else Z_out, t1, t2, r1, r2, gmode, gb, gout, cplx)
@@ -403,7 +411,8 @@ def _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx):
     dev = (Z_in if Z_in is not None else Z_out).device
     dt = torch.complex128 if cplx else torch.float64
     Z = Z_out if Z_out is not None else empty_block(n, p, dev, dt)
-    blocks = [(c0, min(p, c0 + MAX_P)) for c0 in range(0, p, MAX_P)]
+    mp = MAX_P_C if cplx else MAX_P
+    blocks = [(c0, min(p, c0 + mp)) for c0 in range(0, p, mp)]
     # 1) z = Zin + terms, column block by column block
     for c0, c1 in blocks:
         sub_terms = [(X, S[:, c0:c1], al) for X, S, al in terms]
@@ -465,7 +474,8 @@ def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch
 def chol(G: torch.Tensor, R: torch.Tensor, status: torch.Tensor, cond_tol: float):
     p = G.shape[0]
     e0 = _t0()
-    rc = lib().rg_chol_f64(p, _coef(G).data_ptr(), R.data_ptr(), status.data_ptr(), float(cond_tol), stream_ptr())
+    fn = lib().rg_chol_c128 if G.dtype == torch.complex128 else lib().rg_chol_f64
+    rc = fn(p, _coef(G).data_ptr(), R.data_ptr(), status.data_ptr(), float(cond_tol), stream_ptr())
     _lib.check(rc, "chol")
     _t1(e0, "rg_chol", 0)
 
