@@ -43,8 +43,11 @@ class ArnoldiFactorization:
     m        : completed block steps
     """
 
-    def __init__(self, n: int, L: int, m_max: int, k: int, rank_tol: float, seed: int, device=None):
+    def __init__(self, n: int, L: int, m_max: int, k: int, rank_tol: float, seed: int, device=None,
+                 dtype=torch.float64):
         self.n = n
+        self.dtype = dtype
+        npdt = np.complex128 if dtype == torch.complex128 else np.float64
         self.L = L
         self.m_max = m_max
         self.k = k
@@ -52,19 +55,19 @@ class ArnoldiFactorization:
         self.m = 0
         dev = _dev.require_cuda(device)
         self.device = dev
-        self._W = _dev.empty_block(n, (m_max + 1) * L, dev)
-        self._H = np.zeros(((m_max + 1) * L, m_max * L))
-        self._F = np.zeros((k, m_max * L))
-        self.z_bar = np.zeros((L, L))
+        self._W = _dev.empty_block(n, (m_max + 1) * L, dev, dtype)
+        self._H = np.zeros(((m_max + 1) * L, m_max * L), dtype=npdt)
+        self._F = np.zeros((k, m_max * L), dtype=npdt)
+        self.z_bar = np.zeros((L, L), dtype=npdt)
         self.breakdown_events: list[str] = []
         self._rng = np.random.default_rng(seed)
-        self._ahat = _dev.empty_block(n, L, dev)
+        self._ahat = _dev.empty_block(n, L, dev, dtype)
         # packed small coefficients of one step: S1 | c1 | S2 | c2 (column-major blocks)
         wmax = (m_max + 1) * L
-        self._coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=torch.float64, device=dev)
+        self._coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=dtype, device=dev)
         self._coef_host = torch.zeros_like(self._coef, device="cpu").pin_memory()
-        self._qr = QrScratch(L, dev)
-        self._qr_host = torch.zeros(5 * L * L, dtype=torch.float64).pin_memory()
+        self._qr = QrScratch(L, dev, dtype)
+        self._qr_host = torch.zeros(5 * L * L, dtype=dtype).pin_memory()
         self._st_host = torch.zeros(2, dtype=torch.int32).pin_memory()
         self.launches = 0  # rg_* kernel launches issued by start/step (diagnostics)
 
@@ -111,20 +114,25 @@ class ArnoldiFactorization:
 
     def _unit_vector_into(self, col: torch.Tensor, v: torch.Tensor, nrm: float):
         """col = v / nrm (division on the device, as the reference's v / nrm)."""
-        r = torch.full((1, 1), nrm, dtype=torch.float64, device=self.device)
+        r = torch.full((1, 1), nrm, dtype=self.dtype, device=self.device)
         _dev.tall(v, col, r1=r)
 
     def _random_direction(self, bases, tries=3):
         """Seeded replacement direction: host PCG64 normals (same stream as the
         reference), CGS twice against ``bases`` on the device.  Returns
         (vector, norm) or (None, 0)."""
-        scratch = [torch.zeros(b.shape[1], dtype=torch.float64, device=self.device).view(-1, 1) for b in bases]
+        scratch = [torch.zeros(b.shape[1], dtype=self.dtype, device=self.device).view(-1, 1) for b in bases]
         part = _dev.get_part()
+        cplx = self.dtype == torch.complex128
         for _ in range(tries):
-            if part is None:
-                draw = self._rng.standard_normal(self.n)
-            else:  # same global stream as one process, sliced to this rank's rows
-                draw = self._rng.standard_normal(part.n)[part.r0:part.r1]
+            n_glob = self.n if part is None else part.n
+            if cplx:  # complex normal: (re, im) pairs from the same stream
+                g = self._rng.standard_normal((n_glob, 2))
+                draw = g[:, 0] + 1j * g[:, 1]
+            else:
+                draw = self._rng.standard_normal(n_glob)
+            if part is not None:  # same global stream as one process, sliced to this rank's rows
+                draw = draw[part.r0:part.r1]
             v = _dev.to_device_block(draw.reshape(-1, 1))
             for _pass in range(2):
                 project_chain(v, v, bases, [s[: b.shape[1]] for s, b in zip(scratch, bases)])
@@ -143,7 +151,7 @@ def _as_block_on(x, dev):
         if x.dim() != 2:
             raise ShapeError(f"expected a vector or 2-D block, got ndim={x.dim()}")
         return _dev.to_device_block(x, dev)
-    a = np.asarray(x, dtype=np.float64)
+    a = np.asarray(x, dtype=np.complex128 if np.iscomplexobj(x) else np.float64)
     if a.ndim == 1:
         a = a.reshape(-1, 1)
     if a.ndim != 2:
@@ -162,7 +170,7 @@ def _apply_operator(opA, Z: torch.Tensor, out: torch.Tensor):
         return
     Y = opA(Z)
     if not isinstance(Y, torch.Tensor):
-        Y = _dev.to_device_block(np.asarray(Y, dtype=np.float64), Z.device)
+        Y = _dev.to_device_block(np.asarray(Y), Z.device)
     if Y.dim() == 1:
         Y = Y.reshape(-1, 1)
     if tuple(Y.shape) != tuple(out.shape):
@@ -185,7 +193,9 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     if norm0 == 0.0 or not np.isfinite(norm0):
         raise ZeroStartBlock("starting block is numerically zero")
     k = recycle.k if recycle is not None else 0
-    fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev)
+    if recycle is not None and recycle.c_device().dtype != R0d.dtype:
+        R0d = R0d.to(recycle.c_device().dtype) if R0d.dtype == torch.float64 else R0d
+    fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev, R0d.dtype)
     V1 = fact.v_block(0)
     qr = _block_qr(fact, R0d, V1)
     fact.z_bar = qr[0]
@@ -209,7 +219,7 @@ def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_r
     """Thin QR X -> Q (Q must not alias X).  Returns (R, flagged)."""
     L = X.shape[1]
     scr = fact._qr
-    if L <= _dev.MAX_P:
+    if L <= _dev.max_p(X):
         cholqr2_launch(X, Q, scr, g1_ready=g1_ready)
         fact._qr_host.copy_(scr.buf, non_blocking=True)
         fact._st_host.copy_(scr.status, non_blocking=True)
@@ -218,8 +228,9 @@ def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_r
         if ok:
             return R, _flags(R, norm_x, fact.rank_tol)
     else:
-        _dev.tall(X, None, gram=("sumsq", scr.buf[:L]))
-        norm_x = float(np.sqrt(scr.buf[:L].sum().item()))
+        ss = torch.empty(L, dtype=torch.float64, device=X.device)
+        _dev.tall(X, None, gram=("sumsq", ss))
+        norm_x = float(np.sqrt(ss.sum().item()))
     tsqr_into(X, Q, scr)
     R = np.triu(scr.RT.cpu().numpy())
     return R, _flags(R, norm_x, fact.rank_tol)
@@ -242,7 +253,7 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     Vnew = fact.v_block(m + 1)
 
     if ortho == "cgs2":
-        if _dev.fused_ok() and L <= _dev.MAX_P and fact.k + (m + 1) * L <= 256:
+        if _dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P and fact.k + (m + 1) * L <= 256:
             # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64)
             _dev.cgs2(Ahat, C, active, fact._coef, scr.G1)
         else:
@@ -251,10 +262,10 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
                 bases, coefs = [C, active, C, active], [S1, c1, S2, c2]
             else:
                 bases, coefs = [active, active], [c1, c2]
-            project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.MAX_P else None)
+            project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.max_p(Ahat) else None)
         ncoef = (2 * fact.k + 2 * (m + 1) * L) * L
         fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
-        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.MAX_P)
+        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.max_p(Ahat))
         hc = fact._coef_host.numpy()
         k, w = fact.k, (m + 1) * L
         off = 0
@@ -295,7 +306,7 @@ def _mgs_project(fact, Ahat, C, m, cols):
     if C is not None:
         bases += [C[:, i: i + 1] for i in range(C.shape[1])]
     bases += [fact.v_block(i) for i in range(m + 1)]
-    coef = torch.zeros(sum(b.shape[1] for b in bases) * L, dtype=torch.float64, device=fact.device)
+    coef = torch.zeros(sum(b.shape[1] for b in bases) * L, dtype=fact.dtype, device=fact.device)
     views, off = [], 0
     for b in bases:
         a = b.shape[1]

@@ -55,16 +55,29 @@ def _flags(r: np.ndarray, norm_x: float, rank_tol: float) -> np.ndarray:
     return np.abs(np.diagonal(r)) <= rank_tol * max(norm_x, np.finfo(float).tiny)
 
 
+def _phase(d: np.ndarray) -> np.ndarray:
+    """Unit factors making a diagonal real and >= 0: the sign for real data
+    (dense_kernels.py:42-45), the phase for complex data."""
+    if np.iscomplexobj(d):
+        a = np.abs(d)
+        return np.where(a == 0, 1.0 + 0.0j, d / np.where(a == 0, 1.0, a))
+    return np.where(d < 0.0, -1.0, 1.0)
+
+
+def _host_dtype(X):
+    return np.complex128 if np.iscomplexobj(X) else np.float64
+
+
 def host_small_qr(X, rank_tol: float = 1e-12) -> QrFactors:
     """LAPACK thin QR of a SMALL host matrix (recycling.py:157 problems)."""
-    X = np.atleast_2d(np.asarray(X, dtype=np.float64))
+    X = np.atleast_2d(np.asarray(X, dtype=_host_dtype(X)))
     n, L = X.shape
     if n < L:
         raise ValueError(f"reduced_qr needs n >= L, got {n} < {L}")
     q, r = np.linalg.qr(X, mode="reduced")
-    s = np.where(np.diagonal(r) < 0.0, -1.0, 1.0)
+    s = _phase(np.diagonal(r))
     q = np.asfortranarray(q * s)
-    r = r * s[:, None]
+    r = np.conj(s)[:, None] * r
     flagged = _flags(r, float(np.linalg.norm(X)), rank_tol)
     return QrFactors(q=q, r_factor=r, rank=int(L - flagged.sum()), flagged=flagged)
 
@@ -72,10 +85,11 @@ def host_small_qr(X, rank_tol: float = 1e-12) -> QrFactors:
 class QrScratch:
     """Device buffers of one CholQR2 / TSQR (reused across calls)."""
 
-    def __init__(self, L: int, device):
+    def __init__(self, L: int, device, dtype=torch.float64):
         self.L = L
+        self.dtype = dtype
         # packed: G1 | R1 | G2 | R2 | R_tsqr  (each L x L, column-major) + 2 status ints
-        self.buf = torch.zeros(5 * L * L, dtype=torch.float64, device=device)
+        self.buf = torch.zeros(5 * L * L, dtype=dtype, device=device)
         self.status = torch.zeros(2, dtype=torch.int32, device=device)
 
     def mat(self, i: int) -> torch.Tensor:
@@ -93,7 +107,7 @@ def cholqr2_launch(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch, g1_ready: b
     """Enqueue CholQR2 of X into Q (Q may not alias X: X is kept intact for
     the TSQR fallback).  If ``g1_ready``, scr.G1 already holds X^T X (fused
     into the producing pass)."""
-    if _dev.fused_ok() and X.shape[1] <= _dev.MAX_P:
+    if _dev.fused_ok() and X.shape[1] <= _dev.MAX_P and X.dtype == torch.float64:
         # G1 | R1 | G2 | R2 are the first four blocks of scr.buf, as rg_cholqr2_f64 expects
         _dev.cholqr2(X, Q, scr.buf, scr.status, g1_ready)
         return
@@ -109,7 +123,7 @@ def cholqr2_finish(host_buf: np.ndarray, host_status: np.ndarray, L: int):
     """Host side after the D2H copy: (ok, R, ||X||_F)."""
     mats = host_buf.reshape(5, L, L).transpose(0, 2, 1)  # column-major -> row-major views
     G1, R1, _, R2 = mats[0], mats[1], mats[2], mats[3]
-    norm_x = float(np.sqrt(max(np.trace(G1), 0.0)))
+    norm_x = float(np.sqrt(max(np.trace(G1).real, 0.0)))
     ok = bool(host_status[0] == 0 and host_status[1] == 0)
     R = np.triu(R2 @ R1) if ok else None
     return ok, R, norm_x
@@ -122,6 +136,9 @@ def tsqr_into(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch) -> None:
     all-gathered, the stack is factored on every rank (identical input,
     identical LAPACK result), and each rank applies its block of the small Q
     to its rows (Q_local <- Q_local S_rank, one rg_tall pass)."""
+    if X.dtype == torch.complex128:
+        _shifted_cholqr3(X, Q, scr)
+        return
     if Q.data_ptr() != X.data_ptr():
         Q.copy_(X)
     _dev.tsqr(Q, scr.RT)
@@ -133,6 +150,35 @@ def tsqr_into(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch) -> None:
     S = torch.from_numpy(S_rank).to(Q.device)
     _dev.tall(None, Q, [(Q, S, 1.0)], n=Q.shape[0], p=L)
     scr.RT.copy_(torch.from_numpy(np.asfortranarray(rs)).to(Q.device))
+
+
+def _shifted_cholqr3(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch) -> None:
+    """Robust thin QR without Householder (used for complex blocks, whose
+    TSQR is not implemented): shifted CholQR on X, then CholQR2 on the
+    result (Fukaya et al.'s shifted CholQR3).  R = R3 R2 R1 lands in scr.RT."""
+    n, L = X.shape
+    dt = X.dtype
+    dev = X.device
+    G = _dev.small(L, L, dev, dt)
+    _dev.tall(X, None, gram=("self", G))
+    Gh = G.cpu().numpy()
+    nrm2 = float(np.trace(Gh).real)
+    shift = 11.0 * (n * L + L * (L + 1)) * np.finfo(float).eps * max(nrm2, np.finfo(float).tiny)
+    Gs = torch.from_numpy(np.asfortranarray(Gh + shift * np.eye(L))).to(dev)
+    Rs = []
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    cur = X
+    for stage in range(3):
+        R = _dev.small(L, L, dev, dt)
+        if stage > 0:
+            Gs = _dev.small(L, L, dev, dt)
+            _dev.tall(cur, None, gram=("self", Gs))
+        _dev.chol(Gs, R, st, 0.0)
+        _dev.tall(cur, Q, r1=R)
+        cur = Q
+        Rs.append(np.triu(R.cpu().numpy()))
+    Rt = Rs[2] @ Rs[1] @ Rs[0]
+    scr.RT.copy_(torch.from_numpy(np.asfortranarray(np.triu(Rt))).to(dev))
 
 
 def tsqr_combine(R_local: np.ndarray, comm):
@@ -162,18 +208,21 @@ def _wide_qr(X: torch.Tensor, Q: torch.Tensor, rank_tol: float) -> QrFactors:
     ss = torch.zeros(L, dtype=torch.float64, device=X.device)
     _dev.tall(Q, None, gram=("sumsq", ss))
     norm_x = float(np.sqrt(ss.sum().item()))
-    R = np.zeros((L, L))
+    cplx = X.dtype == torch.complex128
+    R = np.zeros((L, L), dtype=np.complex128 if cplx else np.float64)
     from .ortho import project_chain
 
-    for b0 in range(0, L, TSQR_MAX_P):
-        b1 = min(L, b0 + TSQR_MAX_P)
+    panel = _dev.MAX_P_C if cplx else TSQR_MAX_P
+    for b0 in range(0, L, panel):
+        b1 = min(L, b0 + panel)
         Qb = Q[:, b0:b1]
         if b0:
             prev = Q[:, :b0]
-            c1, c2 = _dev.small(b0, b1 - b0, X.device), _dev.small(b0, b1 - b0, X.device)
+            c1 = _dev.small(b0, b1 - b0, X.device, X.dtype)
+            c2 = _dev.small(b0, b1 - b0, X.device, X.dtype)
             project_chain(Qb, Qb, [prev, prev], [c1, c2])
             R[:b0, b0:b1] = c1.cpu().numpy() + c2.cpu().numpy()
-        scr = QrScratch(b1 - b0, X.device)
+        scr = QrScratch(b1 - b0, X.device, X.dtype)
         tsqr_into(Qb, Qb, scr)
         R[b0:b1, b0:b1] = np.triu(scr.RT.cpu().numpy())
     flagged = _flags(R, norm_x, rank_tol)
@@ -187,14 +236,15 @@ def reduced_qr_device(X: torch.Tensor, rank_tol: float = 1e-12, Q: torch.Tensor 
     if n < L:
         raise ValueError(f"reduced_qr needs n >= L, got {n} < {L}")
     dev = X.device
+    cplx = X.dtype == torch.complex128
     if Q is None:
-        Q = _dev.empty_block(n, L, dev)
-    if L > TSQR_MAX_P:
+        Q = _dev.empty_block(n, L, dev, X.dtype)
+    if L > (_dev.MAX_P_C if cplx else TSQR_MAX_P):
         return _wide_qr(X, Q, rank_tol)
-    if scr is None or scr.L != L:
-        scr = QrScratch(L, dev)
+    if scr is None or scr.L != L or scr.dtype != X.dtype:
+        scr = QrScratch(L, dev, X.dtype)
     in_place = Q.data_ptr() == X.data_ptr()
-    if L <= _dev.MAX_P and not in_place:
+    if L <= (_dev.MAX_P_C if cplx else _dev.MAX_P) and not in_place:
         cholqr2_launch(X, Q, scr)
         hb = scr.buf.cpu().numpy()
         hs = scr.status.cpu().numpy()
@@ -203,8 +253,9 @@ def reduced_qr_device(X: torch.Tensor, rank_tol: float = 1e-12, Q: torch.Tensor 
             flagged = _flags(R, norm_x, rank_tol)
             return QrFactors(q=Q, r_factor=R, rank=int(L - flagged.sum()), flagged=flagged)
     else:
-        _dev.tall(X, None, gram=("sumsq", scr.buf[:L]))
-        norm_x = float(np.sqrt(scr.buf[:L].sum().item()))
+        ss = torch.empty(L, dtype=torch.float64, device=dev)
+        _dev.tall(X, None, gram=("sumsq", ss))
+        norm_x = float(np.sqrt(ss.sum().item()))
     tsqr_into(X, Q, scr)
     R = np.triu(scr.RT.cpu().numpy())
     flagged = _flags(R, norm_x, rank_tol)
@@ -220,7 +271,7 @@ def reduced_qr(X, rank_tol: float = 1e-12) -> QrFactors:
     if isinstance(X, torch.Tensor):
         Xd = _dev.to_device_block(X if X.dim() == 2 else X.reshape(-1, 1))
         return reduced_qr_device(Xd, rank_tol)
-    Xh = np.atleast_2d(np.asarray(X, dtype=np.float64))
+    Xh = np.atleast_2d(np.asarray(X, dtype=_host_dtype(X)))
     n, L = Xh.shape
     if n < L:
         raise ValueError(f"reduced_qr needs n >= L, got {n} < {L}")
@@ -231,7 +282,7 @@ def reduced_qr(X, rank_tol: float = 1e-12) -> QrFactors:
 def solve_triangular(Rf, rhs) -> np.ndarray:
     """Back substitution Rf Y = rhs; a diagonal below 1e-14 * ||Rf|| signals
     breakdown upstream and raises naming the column (dense_kernels.py:51-63)."""
-    Rf = np.asarray(Rf, dtype=np.float64)
+    Rf = np.asarray(Rf, dtype=_host_dtype(Rf))
     d = np.abs(np.diagonal(Rf))
     bad = np.flatnonzero(d <= 1e-14 * max(np.linalg.norm(Rf), np.finfo(float).tiny))
     if bad.size:
@@ -256,7 +307,7 @@ class ProgressiveBlockLs:
     without solving for Y."""
 
     def __init__(self, L: int, g0: np.ndarray):
-        g0 = np.atleast_2d(np.asarray(g0, dtype=np.float64))
+        g0 = np.atleast_2d(np.asarray(g0, dtype=_host_dtype(g0)))
         if g0.shape[0] != L:
             raise ValueError("g0 must have L rows")
         self.L = L
@@ -268,21 +319,25 @@ class ProgressiveBlockLs:
 
     def append_block(self, new_cols: np.ndarray) -> np.ndarray:
         L, m = self.L, self.m
-        blk = np.array(new_cols, dtype=np.float64, copy=True)
+        dt = np.complex128 if (np.iscomplexobj(new_cols) or np.iscomplexobj(self.g)) else np.float64
+        blk = np.array(new_cols, dtype=dt, copy=True)
         if blk.shape != ((m + 2) * L, L):
             raise ValueError(f"expected new block of shape {((m + 2) * L, L)}, got {blk.shape}")
+        if dt == np.complex128:
+            self.g = self.g.astype(np.complex128)
         for i, Qt in enumerate(self._factors):
             rows = slice(i * L, (i + 2) * L)
             blk[rows] = Qt @ blk[rows]
         win = blk[m * L:, :]
         Qw, Rw = np.linalg.qr(win, mode="complete")  # Qw 2L x 2L
-        s = np.ones(2 * L)
-        s[:L] = np.where(np.diagonal(Rw) < 0.0, -1.0, 1.0)
-        Qt = s[:, None] * Qw.T
+        s = np.ones(2 * L, dtype=dt)
+        s[:L] = _phase(np.diagonal(Rw))
+        # Q^H with the first L rows re-phased: the new diagonal is real >= 0
+        Qt = np.conj(s)[:, None] * np.conj(Qw).T
         blk[m * L:, :] = 0.0
-        blk[m * L:(m + 1) * L, :] = s[:L, None] * Rw[:L]
+        blk[m * L:(m + 1) * L, :] = np.conj(s[:L])[:, None] * Rw[:L]
         self._factors.append(Qt)
-        self.g = np.vstack([self.g, np.zeros((L, self.n_rhs))])
+        self.g = np.vstack([self.g, np.zeros((L, self.n_rhs), dtype=self.g.dtype)])
         self.g[m * L:, :] = Qt @ self.g[m * L:, :]
         for c in range(L):
             self._rcols.append(blk[:(m + 1) * L, c].copy())
@@ -294,7 +349,7 @@ class ProgressiveBlockLs:
 
     def r_factor(self) -> np.ndarray:
         k = self.m * self.L
-        R = np.zeros((k, k))
+        R = np.zeros((k, k), dtype=self.g.dtype)
         for j, col in enumerate(self._rcols):
             R[: j + 1, j] = col[: j + 1]
         return R
@@ -323,7 +378,7 @@ class EigPairs:
     def complex_vector(self, i: int) -> np.ndarray:
         kind = self.pairing[i]
         if kind == 0:
-            return self.vectors[:, i].astype(complex)
+            return self.vectors[:, i].astype(complex)  # (already complex for complex problems)
         if kind == 1:
             return self.vectors[:, i] + 1j * self.vectors[:, i + 1]
         return self.vectors[:, i - 1] - 1j * self.vectors[:, i]
@@ -350,21 +405,24 @@ def _real_basis(w, v) -> EigPairs:
 
 def eig_standard(M) -> EigPairs:
     """All eigenpairs of a small real square matrix (LAPACK dgeev)."""
-    M = np.asarray(M, dtype=np.float64)
+    M = np.asarray(M, dtype=_host_dtype(M))
     if M.ndim != 2 or M.shape[0] != M.shape[1]:
         raise ValueError("eig_standard needs a square matrix")
     try:
         w, v = np.linalg.eig(M)
     except np.linalg.LinAlgError as e:
         raise np.linalg.LinAlgError(f"eigenvalue iteration failed: {e}") from e
+    if np.iscomplexobj(M):
+        # complex problems use the eigenvectors directly (no conjugate pairs)
+        return EigPairs(values=np.asarray(w, dtype=complex), vectors=v, pairing=np.zeros(len(w), dtype=np.int8))
     return _real_basis(w, v)
 
 
 def eig_generalized(Ag, Bg) -> EigPairs:
     """Ag t = theta Bg t via Bg^{-1} Ag; raises SingularMatrixError when
     cond(Bg) > 1e14 (dense_kernels.py:267-282)."""
-    Ag = np.asarray(Ag, dtype=np.float64)
-    Bg = np.asarray(Bg, dtype=np.float64)
+    Ag = np.asarray(Ag, dtype=_host_dtype(Ag) if np.iscomplexobj(Ag) or not np.iscomplexobj(Bg) else np.complex128)
+    Bg = np.asarray(Bg, dtype=Ag.dtype)
     if Ag.shape != Bg.shape or Ag.shape[0] != Ag.shape[1]:
         raise ValueError("eig_generalized needs square matrices of equal size")
     if Bg.size and np.linalg.cond(Bg) > 1e14:

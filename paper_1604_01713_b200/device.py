@@ -125,6 +125,8 @@ def to_device_block(x, device=None, dtype=torch.float64) -> torch.Tensor:
         t = x
         if t.dim() == 1:
             t = t.reshape(-1, 1)
+        if t.is_complex():
+            dtype = torch.complex128
         if t.device == dev and t.dtype == dtype and is_col_major(t):
             return t
         out = empty_block(t.shape[0], t.shape[1], dev, dtype)
@@ -234,6 +236,8 @@ def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: in
     p = X.shape[1]
     n_local = dcsr.n_cols if n_local is None else n_local
     cplx = X.dtype == torch.complex128
+    if cplx != (dcsr.values.dtype == torch.complex128) or Y.dtype != X.dtype:
+        raise TypeError(f"spmm: matrix values {dcsr.values.dtype}, block {X.dtype}, output {Y.dtype} must agree")
     fn = L.rg_spmm_csr_c128 if cplx else L.rg_spmm_csr_f64
     e0 = _t0()
     rc = fn(n_rows, row_begin, row_end, dcsr.row_ptr.data_ptr(), dcsr.col_idx.data_ptr(),
@@ -438,6 +442,11 @@ def _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx):
             tall(zc, None, gram=("basis", Z, gout[:, c0:c1]), n=n, p=c1 - c0)
         else:
             tall(zc, None, gram=("sumsq", gram[1][c0:c1]), n=n, p=c1 - c0)
+
+
+def max_p(t: torch.Tensor) -> int:
+    """Widest block one rg_tall launch handles for this dtype."""
+    return MAX_P_C if t.dtype == torch.complex128 else MAX_P
 
 
 def fused_ok() -> bool:

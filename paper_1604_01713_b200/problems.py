@@ -191,3 +191,24 @@ def stencil27_complex(N: int, sigma: complex = complex(-0.5, 0.3), seed: int = 0
     vals[~dflag] = rng.uniform(-1.0, 0.0, int((~dflag).sum()))
     vals[dflag] = 26.0 + sigma
     return row_ptr.astype(np.int32), col_idx, vals, n
+
+
+def cfg5_sequence(N: int = 160, n_systems: int = 4, p: int = 16):
+    """BASELINE configs[4]: complex 27-point stencil N^3 with p=16 complex
+    N(0,1) right-hand sides, m=8, k=16.  The 4-shift sequence is a builder
+    decision: system i has diagonal 26 + sigma_i with
+    sigma_i = (-0.5 - 0.05 i) + (0.3 + 0.05 i) 1j; tol 1e-8 as config 4.
+    Returns (system(i) -> CsrMatrix, B, solver kwargs)."""
+    rp, ci, v0, n = stencil27_complex(N)
+    diag = np.zeros(len(ci), dtype=bool)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    diag[ci == rows] = True
+    g = np.random.default_rng(0).standard_normal((n, 2 * p))
+    B = np.asfortranarray(g[:, :p] + 1j * g[:, p:])
+
+    def system(i):
+        v = v0.copy()
+        v[diag] = 26.0 + complex(-0.5 - 0.05 * i, 0.3 + 0.05 * i)
+        return CsrMatrix(n, n, rp, ci, v, _validated=True)
+
+    return system, B, dict(m=8, k=16, tol=1e-8, max_cycles=200)

@@ -146,6 +146,11 @@ class CsrMatrix:
         return cls(m.shape[0], m.shape[1], m.indptr.copy(), m.indices.copy(),
                    np.asarray(m.data, dtype=np.float64).copy())
 
+    def astype_complex(self) -> "CsrMatrix":
+        """The same pattern with complex128 values (real matrix, complex blocks)."""
+        return CsrMatrix(self.n_rows, self.n_cols, self.row_ptr, self.col_idx,
+                         self.values.astype(np.complex128), _validated=True)
+
     @property
     def nnz(self) -> int:
         return len(self.values)
