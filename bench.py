@@ -42,12 +42,19 @@ import numpy as np  # noqa: E402
 P_BLOCK, K_RECYCLE, M_STEPS = 8, 20, 10
 SAMPLE_GRID = 64  # CPU sample: 64^3 rows of the same operator family
 
+# operator families of the step workload: cfg4 (real conv-diff, BASELINE
+# configs[3]) and cfg5 (complex 27-point stencil, BASELINE configs[4])
+FAMILIES = {
+    "cfg4": dict(p=8, k=20, m=10, grid=256, esz=8),
+    "cfg5": dict(p=16, k=16, m=8, grid=160, esz=16),
+}
 
-def step_model_bytes(n, nnz, p=P_BLOCK, k=K_RECYCLE, j=M_STEPS - 1):
+
+def step_model_bytes(n, nnz, p=P_BLOCK, k=K_RECYCLE, j=M_STEPS - 1, esz=8):
     w = (j + 1) * p
-    spmm = nnz * 12 + (n + 1) * 4 + 2 * p * n * 8
-    cgs2 = 8 * n * (4 * k + 4 * w + 12 * p)
-    qr = 24 * n * p
+    spmm = nnz * (esz + 4) + (n + 1) * 4 + 2 * p * n * esz
+    cgs2 = esz * n * (4 * k + 4 * w + 12 * p)
+    qr = 3 * esz * n * p
     return spmm + cgs2 + qr, dict(spmm=spmm, cgs2=cgs2, qr=qr)
 
 
@@ -168,7 +175,7 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 
 
-def _setup_step(grid, dev, seed=0, world=1, rank=0):
+def _setup_step(grid, dev, seed=0, world=1, rank=0, family="cfg4"):
     """Operator, recycle space and a 9-step factorisation resident on `dev`.
 
     world > 1: weak scaling -- rank r owns z-planes [r*grid, (r+1)*grid) of a
@@ -183,7 +190,17 @@ def _setup_step(grid, dev, seed=0, world=1, rank=0):
     from paper_1604_01713_b200.solver import _Operator, _scrub
 
     t0 = time.perf_counter()
-    if world == 1:
+    fam = FAMILIES[family]
+    P, K, M = fam["p"], fam["k"], fam["m"]
+    dt = torch.complex128 if family == "cfg5" else torch.float64
+    if family == "cfg5":
+        if world != 1:
+            raise SystemExit("the cfg5 step workload is single-GPU (weak-scaling runs use cfg4)")
+        system, _, _ = problems.cfg5_sequence(N=grid, p=P)
+        A = system(0)
+        op = _Operator(A, None, "none")
+        n, nnz = A.n_rows, A.nnz
+    elif world == 1:
         A = problems.conv_diff_3d(grid, 20.0)
         op = _Operator(A, None, "none")
         n, nnz = A.n_rows, A.nnz
@@ -201,14 +218,14 @@ def _setup_step(grid, dev, seed=0, world=1, rank=0):
     t_gen = time.perf_counter() - t0
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
-    U0 = D.empty_block(n, K_RECYCLE, dev)
-    U0.copy_(torch.randn(n, K_RECYCLE, generator=g, device=dev, dtype=torch.float64))
+    U0 = D.empty_block(n, K, dev, dt)
+    U0.copy_(torch.randn(n, K, generator=g, device=dev, dtype=dt))
     rs = prepare_cross_system(RecycleSpace(u=U0, c=None), op.apply)
-    R0 = D.empty_block(n, P_BLOCK, dev)
-    R0.copy_(torch.randn(n, P_BLOCK, generator=g, device=dev, dtype=torch.float64))
-    R0 = _scrub(R0, D.empty_block(n, P_BLOCK, dev), rs.c)
-    fact = arnoldi.start(op.apply, R0, m_max=M_STEPS, recycle=rs, seed=seed)
-    for _ in range(M_STEPS - 1):
+    R0 = D.empty_block(n, P, dev, dt)
+    R0.copy_(torch.randn(n, P, generator=g, device=dev, dtype=dt))
+    R0 = _scrub(R0, D.empty_block(n, P, dev, dt), rs.c)
+    fact = arnoldi.start(op.apply, R0, m_max=M, recycle=rs, seed=seed)
+    for _ in range(M - 1):
         arnoldi.step(fact, op.apply, recycle=rs)
     torch.cuda.synchronize()
     return (n, nnz), op, rs, fact, t_gen
@@ -217,7 +234,7 @@ def _setup_step(grid, dev, seed=0, world=1, rank=0):
 def _one_step(fact, op, rs):
     from paper_1604_01713_b200 import arnoldi
 
-    fact.m = M_STEPS - 1
+    fact.m = fact.m_max - 1
     arnoldi.step(fact, op.apply, recycle=rs)
 
 
@@ -232,8 +249,10 @@ def run_ours(args, rank, world):
     if world > 1:
         import torch.distributed as dist
 
-    (n, nnz), op, rs, fact, t_gen = _setup_step(args.grid, dev, seed=rank, world=world, rank=rank)
-    model_bytes, parts = step_model_bytes(n, nnz)
+    fam = FAMILIES[args.family]
+    grid = args.grid or fam["grid"]
+    (n, nnz), op, rs, fact, t_gen = _setup_step(grid, dev, seed=rank, world=world, rank=rank, family=args.family)
+    model_bytes, parts = step_model_bytes(n, nnz, fam["p"], fam["k"], fam["m"] - 1, fam["esz"])
 
     for _ in range(args.warmup):
         _one_step(fact, op, rs)
@@ -285,17 +304,24 @@ def run_ours(args, rank, world):
             e2e["d2h_bytes_per_step"] *= world
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and args.family == "cfg4":
         rate, t, info = cpu_step_rate(steps=3, warmup=1)
         cpu = dict(info, value=rate, unit="GB/s")
 
     if rank == 0:
-        line = {"metric": "SpMM+block-orthog HBM GB/s (block Arnoldi step, cfg4 256^3 p=8 k=20 m=10)",
+        if args.family == "cfg4":
+            metric = "SpMM+block-orthog HBM GB/s (block Arnoldi step, cfg4 256^3 p=8 k=20 m=10)"
+            workload = (f"cfg4-step: arnoldi.step #10 of a cycle, {grid}^3 conv-diff beta=20 "
+                        f"per GPU, n={n}, nnz={nnz} per GPU, p=8, k=20, basis 80 cols (cfg3 shapes)")
+        else:
+            metric = "SpMM+block-orthog HBM GB/s (complex block Arnoldi step, cfg5 160^3 p=16 k=16 m=8)"
+            workload = (f"cfg5-step: arnoldi.step #8 of a cycle, {grid}^3 complex 27-point stencil, "
+                        f"n={n}, nnz={nnz}, p=16, k=16, basis 128 cols, complex128")
+        line = {"metric": metric,
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic",
-                "config": {"workload": f"cfg4-step: arnoldi.step #10 of a cycle, {args.grid}^3 conv-diff beta=20 "
-                                       f"per GPU, n={n}, nnz={nnz} per GPU, p=8, k=20, basis 80 cols (cfg3 shapes)",
+                "dtype": "f64" if args.family == "cfg4" else "c128", "data": "synthetic",
+                "config": {"workload": workload,
                            "model_bytes_per_step": model_bytes, "model_parts": parts,
                            "l2": "inputs (>14 GB) far larger than the 126 MB L2; no flush needed",
                            "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU"},
@@ -316,11 +342,13 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
 
     from paper_1604_01713_b200 import device as D
 
-    n, L = fact.n, fact.L
-    wcols = M_STEPS * L
-    hW = torch.empty((wcols, n), dtype=torch.float64).pin_memory()
-    hC = torch.empty((K_RECYCLE, n), dtype=torch.float64).pin_memory()
-    hQ = torch.empty((L, n), dtype=torch.float64).pin_memory()
+    n, L, K = fact.n, fact.L, fact.k
+    dt = fact.dtype
+    esz = 16 if dt == torch.complex128 else 8
+    wcols = fact.m_max * L
+    hW = torch.empty((wcols, n), dtype=dt).pin_memory()
+    hC = torch.empty((K, n), dtype=dt).pin_memory()
+    hQ = torch.empty((L, n), dtype=dt).pin_memory()
     hW.copy_(fact._W[:, :wcols].t())
     hC.copy_(rs.c.t())
     W_dev = fact._W[:, :wcols]
@@ -333,12 +361,12 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
         W_dev.t().copy_(hW, non_blocking=True)
         rs.c.t().copy_(hC, non_blocking=True)
         _one_step(fact, op, rs)
-        hQ.copy_(fact.v_block(M_STEPS).t(), non_blocking=True)
+        hQ.copy_(fact.v_block(fact.m_max).t(), non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    h2d = (wcols + K_RECYCLE) * n * 8
-    d2h = L * n * 8 + (2 * K_RECYCLE + 2 * (wcols + L)) * L * 8 + 5 * L * L * 8
+    h2d = (wcols + K) * n * esz
+    d2h = L * n * esz + (2 * K + 2 * (wcols + L)) * L * esz + 5 * L * L * esz
     return {"value": model_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": "arnoldi.step with basis/C uploaded from pinned host memory and V_11 downloaded each step"}
@@ -362,7 +390,9 @@ def run_solve(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    grid, nsys = args.grid, args.systems
+    if args.family == "cfg5":
+        return _run_solve_cfg5(args, rank, world)
+    grid, nsys = args.grid or 256, args.systems
     t0 = time.perf_counter()
     n_glob = grid ** 3
     B = np.asfortranarray(np.random.default_rng(0).standard_normal((n_glob, P_BLOCK)))
@@ -425,13 +455,53 @@ def run_solve(args, rank, world):
         print(json.dumps(line), flush=True)
 
 
+def _run_solve_cfg5(args, rank, world):
+    """Config-5 sequence (complex 27-point stencil grid^3, p=16, m=8, k=16,
+    4 shifts) on one GPU: time per system."""
+    import torch
+
+    from paper_1604_01713_b200 import SolverConfig, problems, solve_block_gcrodr
+
+    if world != 1:
+        raise SystemExit("the cfg5 solve workload is single-GPU")
+    grid = args.grid or 160
+    nsys = min(args.systems, 4)
+    t0 = time.perf_counter()
+    system, B, kw = problems.cfg5_sequence(N=grid)
+    ops = [system(i) for i in range(nsys)]
+    t_setup = time.perf_counter() - t0
+    cfg = SolverConfig(**kw)
+    rs, per = None, []
+    for i, Ai in enumerate(ops):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        X, rep, rs_out = solve_block_gcrodr(Ai, B, None, cfg, rs_in=rs)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t1
+        rs = rs_out if rs_out is not None else rs
+        per.append({"system": i, "s": dt, "cycles": rep.cycles,
+                    "block_steps": int(sum(len(h) for h in rep.residual_history)),
+                    "matvecs": rep.matvec_count, "converged": bool(rep.converged),
+                    "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms))})
+    mean = statistics.mean(r["s"] for r in per)
+    print(json.dumps({"metric": "GCRO-DR solve s/system (cfg5 complex family)", "value": mean, "unit": "s/system",
+                      "n_gpus": 1, "steps": nsys, "warmup": 0, "ms_per_step": mean * 1e3,
+                      "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+                      "data": "synthetic",
+                      "config": {"workload": f"cfg5 sequence {grid}^3 complex 27-point stencil, p=16, m=8, k=16, "
+                                             f"tol 1e-8, {nsys} shifts", "setup_s": t_setup,
+                                 "parallelism": "1 GPU"},
+                      "systems": per}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--family", choices=sorted(FAMILIES), default="cfg4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--workload", choices=["step", "solve"], default="step")

@@ -109,6 +109,107 @@ spmm_c128_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__
   }
 }
 
+// Production SpMM: no shared-memory staging.  G lanes share a row (G=2
+// splits a 16-wide block into two 8-column halves, so one pass covers p=16
+// and A is read once); each lane walks its own row's entries straight from
+// global memory (L1-resident lines) with the next entry's index/value and X
+// gathers issued one entry ahead.  Rows per warp RPW = 32/G; warps are
+// persistent over RPW-row units.  Arithmetic order is the same as above.
+template <int G, int PB, bool GHOST>
+__global__ void __launch_bounds__(kCWarps * 32, 2)
+spmm_c128_direct_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
+                        const int32_t* __restrict__ ci, const double2* __restrict__ va,
+                        const double2* __restrict__ X, int64_t ldx, int64_t n_local,
+                        const double2* __restrict__ Xg, int64_t ldg, double2* __restrict__ Y, int64_t ldy) {
+  constexpr int RPW = 32 / G;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int rl = lane % RPW;
+  const int cg = lane / RPW;
+  const double2* Xc = X + (int64_t)cg * PB * ldx;
+  const double2* Xgc = GHOST ? Xg + (int64_t)cg * PB * ldg : Xg;
+  double2* Yc = Y + (int64_t)cg * PB * ldy;
+  const int64_t nunits = (row_end - row_begin + RPW - 1) / RPW;
+  const int64_t nwarps = (int64_t)gridDim.x * kCWarps;
+  auto gather = [&](int32_t j, double2 (&xv)[PB]) {
+    const double2* xp = Xc + j;
+    int64_t ld = ldx;
+    if (GHOST && j >= n_local) {
+      xp = Xgc + (j - n_local);
+      ld = ldg;
+    }
+#pragma unroll
+    for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
+  };
+  for (int64_t u = (int64_t)blockIdx.x * kCWarps + w; u < nunits; u += nwarps) {
+    const int64_t i = row_begin + u * RPW + rl;
+    const bool valid = i < row_end;
+    const int32_t t0 = valid ? __ldg(rp + i) : 0;
+    const int32_t t1 = valid ? __ldg(rp + i + 1) : 0;
+    double ar_[PB], ai_[PB];
+#pragma unroll
+    for (int c = 0; c < PB; ++c) ar_[c] = ai_[c] = 0.0;
+    double2 xn[PB];
+    double2 an = make_double2(0.0, 0.0);
+    int32_t jn2 = 0;
+    if (t0 < t1) {
+      an = __ldg(va + t0);
+      gather(__ldg(ci + t0), xn);
+      if (t0 + 1 < t1) jn2 = __ldg(ci + t0 + 1);
+    }
+    for (int32_t t = t0; t < t1; ++t) {
+      double2 xc[PB];
+#pragma unroll
+      for (int c = 0; c < PB; ++c) xc[c] = xn[c];
+      const double2 a = an;
+      if (t + 1 < t1) {
+        an = __ldg(va + t + 1);
+        gather(jn2, xn);
+        if (t + 2 < t1) jn2 = __ldg(ci + t + 2);
+      }
+#pragma unroll
+      for (int c = 0; c < PB; ++c) {
+        const double pr = __dsub_rn(__dmul_rn(a.x, xc[c].x), __dmul_rn(a.y, xc[c].y));
+        const double pi = __dadd_rn(__dmul_rn(a.x, xc[c].y), __dmul_rn(a.y, xc[c].x));
+        ar_[c] = __dadd_rn(ar_[c], pr);
+        ai_[c] = __dadd_rn(ai_[c], pi);
+      }
+    }
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < PB; ++c) Yc[i + c * ldy] = make_double2(ar_[c], ai_[c]);
+    }
+  }
+}
+
+template <int G, int PB>
+static void launch_spmm_cd(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double2* va,
+                           const double2* X, int64_t ldx, int64_t n_local, const double2* Xg, int64_t ldg,
+                           double2* Y, int64_t ldy, cudaStream_t s) {
+  static int per_sm[2] = {-1, -1};
+  const int gi = Xg ? 1 : 0;
+  if (per_sm[gi] < 0) {
+    int v = 0;
+    if (Xg)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_c128_direct_kernel<G, PB, true>, kCWarps * 32, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_c128_direct_kernel<G, PB, false>, kCWarps * 32, 0);
+    per_sm[gi] = v < 1 ? 1 : v;
+  }
+  constexpr int RPW = 32 / G;
+  const int64_t units = (re - rb + RPW - 1) / RPW;
+  int64_t g = (int64_t)sm_count() * per_sm[gi];
+  const int64_t need = (units + kCWarps - 1) / kCWarps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  if (Xg)
+    spmm_c128_direct_kernel<G, PB, true><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                             Xg, ldg, Y, ldy);
+  else
+    spmm_c128_direct_kernel<G, PB, false><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+                                                                              Xg, ldg, Y, ldy);
+}
+
 template <int PB>
 static void launch_spmm_c(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double2* va,
                           const double2* X, int64_t ldx, int64_t n_local, const double2* Xg, int64_t ldg, double2* Y,
@@ -508,6 +609,34 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
   const double2* Xg = reinterpret_cast<const double2*>(d_xg);
   double2* Y = reinterpret_cast<double2*>(d_y);
   const double2* va = reinterpret_cast<const double2*>(d_vals);
+  static const int legacy = getenv("RG_SPMMC_LEGACY") ? 1 : 0;
+  static const int g2_8 = getenv("RG_SPMMC_G2_8") ? 1 : 0;
+  if (!legacy) {
+    // passes of 16 columns (two lanes per row), then one exact-width pass
+    for (int c0 = 0; c0 < p;) {
+      const int rem = p - c0;
+      const int pc = rem >= 16 ? 16 : (rem >= 8 ? 8 : rem);
+      const double2* Xc = X ? X + (int64_t)c0 * ldx : nullptr;
+      const double2* Xgc = Xg ? Xg + (int64_t)c0 * ldg : nullptr;
+      double2* Yc = Y + (int64_t)c0 * ldy;
+#define RG_CD(G, PB) launch_spmm_cd<G, PB>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s)
+      switch (pc) {
+        case 16: RG_CD(2, 8); break;
+        case 8: if (g2_8) RG_CD(2, 4); else RG_CD(1, 8); break;
+        case 7: RG_CD(1, 7); break;
+        case 6: RG_CD(1, 6); break;
+        case 5: RG_CD(1, 5); break;
+        case 4: RG_CD(1, 4); break;
+        case 3: RG_CD(1, 3); break;
+        case 2: RG_CD(1, 2); break;
+        default: RG_CD(1, 1); break;
+      }
+#undef RG_CD
+      RG_CHECK_LAUNCH("rg_spmm_csr_c128");
+      c0 += pc;
+    }
+    return RG_OK;
+  }
   for (int c0 = 0; c0 < p;) {
     const int rem = p - c0;
     const int pc = rem >= 8 ? 8 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));

@@ -17,11 +17,13 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--family", default="cfg4")
     ap.add_argument("--steps", type=int, default=2)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    _, op, rs, fact, _ = bench._setup_step(args.grid, dev)
+    grid = args.grid or bench.FAMILIES[args.family]["grid"]
+    _, op, rs, fact, _ = bench._setup_step(grid, dev, family=args.family)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStart()
     for _ in range(args.steps):
