@@ -592,6 +592,474 @@ __global__ void chol_c128_kernel(int p, const double2* __restrict__ G, double2* 
   }
 }
 
+// ============================================================================
+// tall_c6: complex tall-skinny pass on the FP64 tensor cores (p <= 16)
+//
+// The v6 design of rg_tall.cu in complex form.  A warp owns 32-row units;
+// every n-length operand streams through a per-warp ring of cp.async slabs
+// (32 rows x 4 complex columns, 16-byte chunks straight from the
+// interleaved layout) driven by a per-CTA slab table.  Complex products
+// are four real DMMA m8n8k4 per tile:
+//   update  z += X (alpha S):  zr += Xr Sr' - Xi Si',  zi += Xr Si' + Xi Sr'
+//           A = X slab element (re, im) [row][col], B = pre-arranged S'
+//           fragments (alpha folded in), C = the 32 x p z tile in registers
+//   Gram    G += Gb^H z:  Gr += Gbr zr + Gbi zi,  Gi += Gbr zi - Gbi zr
+//           A = Gb slab pair [col][row], B = the z tile in smem
+// Slab strides (in complex elements) keep every fragment read conflict-free:
+// 34 for [row][col] reads of X / zin slabs, 36 for [col][row] reads of Gb
+// slabs and the z tile.
+// ============================================================================
+
+constexpr int kC6Warps = 8;
+constexpr int kC6Threads = kC6Warps * 32;
+template <int PM>
+struct C6Ring {
+  static constexpr int value = PM > 8 ? 5 : 6;  // slabs in flight per warp (smem-bound)
+};
+constexpr int kC6SX = 34;
+constexpr int kC6SG = 36;
+constexpr int kC6Slot = 4 * kC6SG;  // complex elements per ring slot
+constexpr int kC6MaxSlabs = 96;
+
+struct C6Plan {
+  int nz, n1, n2, ng, total;
+};
+
+struct C6Tab {
+  const double2* ptr[kC6MaxSlabs];
+  int64_t ld[kC6MaxSlabs];
+  int nc[kC6MaxSlabs];
+};
+
+__device__ __forceinline__ void cp_async16c(double2* dst, const double2* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit_c() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait_c() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int PM, int MT, bool TRSM, bool NOTERMS>
+__global__ void __launch_bounds__(kC6Threads, 1) tall_c6_kernel(TallC P, C6Plan L) {
+  constexpr int kC6Ring = C6Ring<PM>::value;
+  constexpr int NT = PM / 8;
+  constexpr int MTA = MT > 0 ? MT : 1;
+  constexpr int kWarpC = kC6Ring * kC6Slot + PM * kC6SG;  // complex elements per warp
+  extern __shared__ __align__(16) double smem[];
+  __shared__ C6Tab tab;
+  const int p = P.p;
+  const int ks1 = (P.a1 + 3) / 4, ks2 = (P.a2 + 3) / 4;
+  double2* sf1 = reinterpret_cast<double2*>(smem);  // [ks1][NT][32] (re, im) B fragments of alpha1 S1
+  double2* sf2 = sf1 + (size_t)ks1 * NT * 32;
+  double2* sR1 = sf2 + (size_t)ks2 * NT * 32;       // PM x PM row-major, diagonal slot = 1 / r_jj
+  double2* sR2 = sR1 + PM * PM;
+  double2* wbase = sR2 + PM * PM;
+  double* red = reinterpret_cast<double*>(wbase + (size_t)kC6Warps * kWarpC);
+
+  for (int e = threadIdx.x; e < ks1 * NT * 32; e += kC6Threads) {
+    const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
+    const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
+    double2 v = make_double2(0.0, 0.0);
+    if (aa < P.a1 && c < p) {
+      v = P.s1[aa + (int64_t)c * P.a1];
+      v.x *= P.alpha1;
+      v.y *= P.alpha1;
+    }
+    sf1[e] = v;
+  }
+  for (int e = threadIdx.x; e < ks2 * NT * 32; e += kC6Threads) {
+    const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
+    const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
+    double2 v = make_double2(0.0, 0.0);
+    if (aa < P.a2 && c < p) {
+      v = P.s2[aa + (int64_t)c * P.a2];
+      v.x *= P.alpha2;
+      v.y *= P.alpha2;
+    }
+    sf2[e] = v;
+  }
+  for (int e = threadIdx.x; e < PM * PM; e += kC6Threads) {
+    const int ii = e / PM, jj = e % PM;
+    const double2 id = make_double2(ii == jj ? 1.0 : 0.0, 0.0);
+    double2 v1 = id, v2 = id;
+    if (P.r1 && ii < p && jj < p) {
+      v1 = P.r1[ii + (int64_t)jj * p];
+      if (ii == jj) v1 = make_double2(1.0 / v1.x, 0.0);
+    }
+    if (P.r2 && ii < p && jj < p) {
+      v2 = P.r2[ii + (int64_t)jj * p];
+      if (ii == jj) v2 = make_double2(1.0 / v2.x, 0.0);
+    }
+    sR1[e] = v1;
+    sR2[e] = v2;
+  }
+  // two solves z R1^-1 R2^-1 become one with R2 R1 (upper triangular, real
+  // positive diagonal): half the substitution work
+  const bool two = P.r1 && P.r2;
+  if (TRSM && two) {
+    __syncthreads();
+    double2* prod = reinterpret_cast<double2*>(red);  // PM x PM scratch (red is free until the epilogue)
+    for (int e = threadIdx.x; e < PM * PM; e += kC6Threads) {
+      const int ii = e / PM, jj = e % PM;
+      double2 v = make_double2(ii == jj ? 1.0 : 0.0, 0.0);
+      if (ii < p && jj < p) {
+        v = make_double2(0.0, 0.0);
+        for (int k = ii; k <= jj; ++k) {
+          const double2 a = P.r2[ii + (int64_t)k * p], b = P.r1[k + (int64_t)jj * p];
+          v.x = fma(a.x, b.x, fma(-a.y, b.y, v.x));
+          v.y = fma(a.x, b.y, fma(a.y, b.x, v.y));
+        }
+        if (ii == jj) v = make_double2(1.0 / v.x, 0.0);
+      } else if (ii > jj) {
+        v = make_double2(0.0, 0.0);
+      }
+      prod[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < PM * PM; e += kC6Threads) sR1[e] = prod[e];
+  }
+  for (int k = threadIdx.x; k < L.total; k += kC6Threads) {
+    const double2* ptr;
+    int64_t ld;
+    int nc, s;
+    if (k < L.nz) {
+      ptr = P.zin; ld = P.ldzin; s = k; nc = p - s * 4;
+    } else if (k < L.nz + L.n1) {
+      ptr = P.x1; ld = P.ldx1; s = k - L.nz; nc = P.a1 - s * 4;
+    } else if (k < L.nz + L.n1 + L.n2) {
+      ptr = P.x2; ld = P.ldx2; s = k - L.nz - L.n1; nc = P.a2 - s * 4;
+    } else {
+      ptr = P.gb; ld = P.ldgb; s = k - L.nz - L.n1 - L.n2; nc = P.gc - s * 4;
+    }
+    tab.ptr[k] = ptr + (int64_t)(s * 4) * ld;
+    tab.ld[k] = ld;
+    tab.nc[k] = nc > 4 ? 4 : nc;
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  double2* ring = wbase + (size_t)warp * kWarpC;  // [kC6Ring][kC6Slot]
+  double2* zt = ring + kC6Ring * kC6Slot;         // [PM][kC6SG]: zt[c * kC6SG + row]
+  const bool gram_tile = MT > 0 && (P.gmode == 1 || P.gmode == 2);
+  const int mtiles = P.mtiles;
+  const int gfirst = L.nz + L.n1 + L.n2;
+
+  double acc[MTA][NT][2][2];
+#pragma unroll
+  for (int mt = 0; mt < MTA; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0][0] = acc[mt][nt][0][1] = acc[mt][nt][1][0] = acc[mt][nt][1][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  const int64_t nunits = (P.n + 31) / 32;
+  const int64_t gwarp = (int64_t)blockIdx.x * kC6Warps + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * kC6Warps;
+  const int64_t my_units = gwarp < nunits ? (nunits - gwarp + nwarps - 1) / nwarps : 0;
+
+  int64_t iss_left = my_units * L.total;
+  int64_t iss_r0 = gwarp * 32;
+  int iss_k = 0, iss_slot = 0;
+  auto issue_next = [&]() {
+    if (iss_left > 0) {
+      const double2* base = tab.ptr[iss_k];
+      const int64_t ld = tab.ld[iss_k];
+      const int nc = tab.nc[iss_k];
+      const int st = iss_k >= gfirst ? kC6SG : kC6SX;
+      const bool vrow = iss_r0 + lane < P.n;
+      double2* dst = ring + iss_slot * kC6Slot + lane;
+      const double2* src = base + iss_r0 + lane;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int bytes = (t < nc && vrow) ? 16 : 0;
+        cp_async16c(dst + t * st, bytes ? src + (int64_t)t * ld : base, bytes);
+      }
+      --iss_left;
+      if (++iss_k == L.total) {
+        iss_k = 0;
+        iss_r0 += nwarps * 32;
+      }
+    }
+    cp_commit_c();
+    if (++iss_slot == kC6Ring) iss_slot = 0;
+  };
+#pragma unroll
+  for (int s = 0; s < kC6Ring; ++s) issue_next();
+  int cons_slot = 0;
+  auto take = [&]() -> const double2* {
+    const double2* sl = ring + cons_slot * kC6Slot;
+    if (++cons_slot == kC6Ring) cons_slot = 0;
+    return sl;
+  };
+  auto acquire = [&]() -> const double2* {
+    cp_wait_c<kC6Ring - 1>();
+    __syncwarp();
+    return take();
+  };
+  auto release = [&]() {
+    __syncwarp();
+    issue_next();
+  };
+
+  for (int64_t ui = 0; ui < my_units; ++ui) {
+    const int64_t r0 = (gwarp + ui * nwarps) * 32;
+    // z in DMMA C layout: rows rg*8 + mrow, columns nt*8 + 2*kq + v; [re/im]
+    double zf[4][NT][2][2];
+#pragma unroll
+    for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) zf[rg][nt][0][0] = zf[rg][nt][0][1] = zf[rg][nt][1][0] = zf[rg][nt][1][1] = 0.0;
+    if (NOTERMS) {
+      // no update terms: zin slabs go straight into the z tile (row per lane)
+#pragma unroll
+      for (int k = 0; k < 2 * NT; ++k) {
+        if (k < L.nz) {
+          const double2* sl = acquire();
+#pragma unroll
+          for (int t = 0; t < 4; ++t) zt[(4 * k + t) * kC6SG + lane] = sl[t * kC6SX + lane];
+          release();
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) zt[(4 * k + t) * kC6SG + lane] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncwarp();
+    }
+    // zin slab k holds complex columns 4k..4k+3 = tile k/2, lanes with kq/2 == k%2
+#pragma unroll
+    for (int k = 0; k < 2 * NT; ++k) {
+      if (NOTERMS) break;
+      if (k < L.nz) {
+        const double2* sl = acquire();
+        if ((kq >> 1) == (k & 1)) {
+#pragma unroll
+          for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const double2 e = sl[(2 * (kq & 1) + v) * kC6SX + rg * 8 + mrow];
+              zf[rg][k >> 1][0][v] = e.x;
+              zf[rg][k >> 1][1][v] = e.y;
+            }
+        }
+        release();
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (NOTERMS) break;
+      const int nsl = t == 0 ? L.n1 : L.n2;
+      const double2* sf = t == 0 ? sf1 : sf2;
+      for (int s = 0; s < nsl; ++s) {
+        const double2* sl = acquire();
+        double br[NT], bi[NT], bn[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const double2 b = sf[(s * NT + nt) * 32 + lane];
+          br[nt] = b.x;
+          bi[nt] = b.y;
+          bn[nt] = -b.y;
+        }
+#pragma unroll
+        for (int rg = 0; rg < 4; ++rg) {
+          const double2 a = sl[kq * kC6SX + rg * 8 + mrow];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma_c(zf[rg][nt][0][0], zf[rg][nt][0][1], a.x, br[nt]);
+            dmma_c(zf[rg][nt][0][0], zf[rg][nt][0][1], a.y, bn[nt]);
+            dmma_c(zf[rg][nt][1][0], zf[rg][nt][1][1], a.x, bi[nt]);
+            dmma_c(zf[rg][nt][1][0], zf[rg][nt][1][1], a.y, br[nt]);
+          }
+        }
+        release();
+      }
+    }
+    // ---------------- rows: tile, triangular solves, store, norms
+    if (!NOTERMS) {
+#pragma unroll
+      for (int rg = 0; rg < 4; ++rg)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            zt[(nt * 8 + 2 * kq + v) * kC6SG + rg * 8 + mrow] = make_double2(zf[rg][nt][0][v], zf[rg][nt][1][v]);
+      __syncwarp();
+    }
+    const int64_t i = r0 + lane;
+    const bool valid = i < P.n;
+    if (TRSM) {
+      // lane-per-row forward substitution
+      double zr[PM], zi[PM];
+#pragma unroll
+      for (int c = 0; c < PM; ++c) {
+        const double2 e = zt[c * kC6SG + lane];
+        zr[c] = e.x;
+        zi[c] = e.y;
+      }
+      if (P.r1) ctrsm<PM>(zr, zi, sR1, p);
+      if (P.r2 && !two) ctrsm<PM>(zr, zi, sR2, p);
+#pragma unroll
+      for (int c = 0; c < PM; ++c) zt[c * kC6SG + lane] = make_double2(zr[c], zi[c]);
+      __syncwarp();
+    }
+    if (P.zout && valid) {
+      for (int c = 0; c < p; ++c) P.zout[i + (int64_t)c * P.ldzout] = zt[c * kC6SG + lane];
+    }
+    if (P.gmode == 3 && valid) {
+#pragma unroll
+      for (int c = 0; c < PM; ++c) {
+        const double2 e = zt[c * kC6SG + lane];
+        sq[c] = fma(e.x, e.x, fma(e.y, e.y, sq[c]));
+      }
+    }
+    if (!gram_tile) continue;
+#pragma unroll
+    for (int mt = 0; mt < MTA; ++mt) {
+      if (mt < mtiles) {
+        const double2* sa = zt + (size_t)(mt * 8) * kC6SG;  // self Gram: A = z columns mt*8..
+        int sa_off = mrow * kC6SG;
+        if (P.gmode == 1) {
+          // both slabs of this 8-column Gb tile must have landed
+          cp_wait_c<kC6Ring - 2>();
+          __syncwarp();
+          const double2* s0 = take();
+          const double2* s1 = take();
+          sa = mrow < 4 ? s0 : s1;
+          sa_off = (mrow & 3) * kC6SG;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const double2 a = sa[sa_off + ks * 4 + kq];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const double2 b = zt[(nt * 8 + mrow) * kC6SG + ks * 4 + kq];
+            dmma_c(acc[mt][nt][0][0], acc[mt][nt][0][1], a.x, b.x);
+            dmma_c(acc[mt][nt][0][0], acc[mt][nt][0][1], a.y, b.y);
+            dmma_c(acc[mt][nt][1][0], acc[mt][nt][1][1], a.x, b.y);
+            dmma_c(acc[mt][nt][1][0], acc[mt][nt][1][1], -a.y, b.x);
+          }
+        }
+        if (P.gmode == 1) {
+          release();
+          release();
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cp_wait_c<0>();
+
+  // ---------------- epilogue: deterministic reductions (as tall_c128_kernel)
+  __shared__ bool s_last;
+  __syncthreads();
+  if (gram_tile) {
+    for (int ww = 0; ww < kC6Warps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int ri = 0; ri < 2; ++ri)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                  const int idx = ((((mt * NT + nt) * 2 + ri) * 32) + lane) * 2 + v;
+                  red[idx] = (ww == 0) ? acc[mt][nt][ri][v] : red[idx] + acc[mt][nt][ri][v];
+                }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kC6Threads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[((int64_t)blockIdx.x * ne + e) * 2] = red[((((mt * NT + nt) * 2 + 0) * 32) + ln) * 2 + v];
+      P.part[((int64_t)blockIdx.x * ne + e) * 2 + 1] = red[((((mt * NT + nt) * 2 + 1) * 32) + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+#pragma unroll
+    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kC6Threads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kC6Warps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (P.gmode == 3) {
+    double* out = reinterpret_cast<double*>(P.gout);
+    for (int e = threadIdx.x; e < p; e += kC6Threads) {
+      double sum = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * p + e);
+      out[e] = sum;
+    }
+  } else {
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kC6Threads) {
+      double sr = 0.0, si = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        sr += __ldcg(P.part + ((int64_t)b * ne + e) * 2);
+        si += __ldcg(P.part + ((int64_t)b * ne + e) * 2 + 1);
+      }
+      P.gout[e] = make_double2(sr, si);
+    }
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+template <int PM, int MT>
+static cudaError_t launch_c6(const TallC& P, cudaStream_t st) {
+  constexpr int kC6Ring = C6Ring<PM>::value;
+  constexpr int NT = PM / 8;
+  constexpr int kWarpC = kC6Ring * kC6Slot + PM * kC6SG;
+  const bool trsm = P.r1 || P.r2;
+  const bool noterms = P.a1 == 0 && P.a2 == 0;
+  auto k = trsm ? (noterms ? tall_c6_kernel<PM, MT, true, true> : tall_c6_kernel<PM, MT, true, false>)
+                : (noterms ? tall_c6_kernel<PM, MT, false, true> : tall_c6_kernel<PM, MT, false, false>);
+  const int ki = (trsm ? 2 : 0) + (noterms ? 1 : 0);
+  C6Plan L;
+  L.nz = P.zin ? (P.p + 3) / 4 : 0;
+  L.n1 = (P.a1 + 3) / 4;
+  L.n2 = (P.a2 + 3) / 4;
+  L.ng = P.gmode == 1 ? 2 * P.mtiles : 0;
+  L.total = L.nz + L.n1 + L.n2 + L.ng;
+  const size_t smem = ((size_t)(L.n1 + L.n2) * NT * 32 + 2 * PM * PM + (size_t)kC6Warps * kWarpC) * 16 +
+                      (size_t)std::max(std::max(MT * NT * 2 * 64, kC6Warps * PM), 2 * PM * PM) * sizeof(double);
+  static bool cfg[4] = {false, false, false, false};
+  if (!cfg[ki]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cfg[ki] = true;
+  }
+  const int64_t nunits = (P.n + 31) / 32;
+  int64_t g = (int64_t)sm_count();
+  const int64_t need = (nunits + kC6Warps - 1) / kC6Warps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kC6Threads, smem, st>>>(P, L);
+  return cudaGetLastError();
+}
+
 }  // namespace rg
 
 extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_row_ptr,
@@ -673,13 +1141,15 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
                             void* stream) {
   using namespace rg;
   clear_error();
-  RG_REQUIRE(n >= 0 && p >= 1 && p <= 8, "rg_tall_c128: p=%d outside [1, 8]", p);
-  RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= 256, "rg_tall_c128: term widths %d, %d", a1, a2);
+  RG_REQUIRE(n >= 0 && p >= 1 && p <= 16, "rg_tall_c128: p=%d outside [1, 16]", p);
+  RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= (p > 8 ? 128 : 256), "rg_tall_c128: term widths %d, %d (p=%d)", a1,
+             a2, p);
   RG_REQUIRE(a1 == 0 || (d_x1 && d_s1 && ldx1 >= n), "rg_tall_c128: bad term 1");
   RG_REQUIRE(a2 == 0 || (d_x2 && d_s2 && ldx2 >= n), "rg_tall_c128: bad term 2");
   RG_REQUIRE(gram_mode >= 0 && gram_mode <= 3, "rg_tall_c128: gram_mode %d", gram_mode);
-  RG_REQUIRE(gram_mode != 1 || (d_gb && gc >= 1 && gc <= 48 && ldgb >= n),
-             "rg_tall_c128: Gram basis width gc=%d outside [1, 48]", gc);
+  const int gc_max = p > 8 ? ((a1 == 0 && a2 == 0) ? 64 : 32) : 48;
+  RG_REQUIRE(gram_mode != 1 || (d_gb && gc >= 1 && gc <= gc_max && ldgb >= n),
+             "rg_tall_c128: Gram basis width gc=%d outside [1, %d]", gc, gc_max);
   RG_REQUIRE(gram_mode != 2 || gc == p, "rg_tall_c128: self Gram needs gc == p");
   RG_REQUIRE(gram_mode == 0 || d_gout, "rg_tall_c128: null Gram output");
   if (gram_mode == 3) gc = 1;
@@ -700,6 +1170,25 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
   P.counter = (unsigned*)d_work;
   P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
   if (gram_mode == 0 && n == 0) return RG_OK;
+  cudaStream_t st0 = (cudaStream_t)stream;
+  static const int legacy = getenv("RG_TALLC_LEGACY") ? 1 : 0;
+  if (p > 8 || (p > 4 && !legacy)) {
+    // tensor-core pass (complex v6)
+    cudaError_t e6;
+    const int mt = P.mtiles;
+    if (p > 8) {
+      e6 = mt == 0 ? launch_c6<16, 0>(P, st0)
+                   : (mt <= 2 ? launch_c6<16, 2>(P, st0) : (mt <= 4 ? launch_c6<16, 4>(P, st0) : launch_c6<16, 8>(P, st0)));
+    } else {
+      e6 = mt == 0 ? launch_c6<8, 0>(P, st0)
+                   : (mt <= 2 ? launch_c6<8, 2>(P, st0) : launch_c6<8, 6>(P, st0));
+    }
+    if (e6 != cudaSuccess) {
+      set_error("rg_tall_c128: %s", cudaGetErrorString(e6));
+      return RG_ECUDA;
+    }
+    return RG_OK;
+  }
   const int PM = p <= 1 ? 1 : (p <= 2 ? 2 : (p <= 4 ? 4 : 8));
   const int mtmax = P.mtiles <= 2 ? 2 : 6;
   cudaStream_t st = (cudaStream_t)stream;

@@ -21,9 +21,16 @@ LD_ALIGN = 32
 MAX_P = 16        # block width one rg_tall launch handles
 MAX_GC = 128      # Gram basis columns per launch
 MAX_TERM_COLS = 512
-MAX_P_C = 8       # complex128 limits (rg_tall_c128)
-MAX_GC_C = 48
+MAX_P_C = 16      # complex128 limits (rg_tall_c128); blocks wider than 8 allow
+MAX_GC_C = 48     # a 32-column Gram basis and 128 staged term columns per launch
 MAX_TERM_COLS_C = 256
+
+
+def _c_limits(p: int, has_terms: bool = True):
+    """(max Gram basis columns, max staged term columns) of one complex launch."""
+    if p > 8:
+        return (32 if has_terms else 64), 128
+    return MAX_GC_C, MAX_TERM_COLS_C
 
 
 _COMM = None   # distributed.CommContext when row-partitioned (Gram allreduce)
@@ -349,8 +356,9 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         _zero_gram(gram)
         return
     cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
-    maxp, maxgc = (MAX_P_C, MAX_GC_C) if cplx else (MAX_P, MAX_GC)
-    terms = _split_terms(terms, MAX_TERM_COLS_C if cplx else MAX_TERM_COLS)
+    maxp, maxgc = (MAX_P_C, _c_limits(p, bool(terms))[0]) if cplx else (MAX_P, MAX_GC)
+    tcols = _c_limits(p)[1] if cplx else MAX_TERM_COLS
+    terms = _split_terms(terms, tcols)
     r1 = _coef(r1) if r1 is not None else None
     r2 = _coef(r2) if r2 is not None else None
     if p > maxp:
@@ -368,7 +376,6 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         else:
             raise ValueError(f"unknown gram kind {kind!r}")
     # passes over the term list (<= 2 terms and <= MAX_TERM_COLS staged columns each)
-    tcols = MAX_TERM_COLS_C if cplx else MAX_TERM_COLS
     groups, cur_g, cur_cols = [], [], 0
     for t in terms:
         a = t[0].shape[1]
@@ -380,8 +387,9 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
     if cur_g or not groups:
         groups.append(cur_g)
     needs_multi = len(groups) > 1 or (gmode == 1 and gb.shape[1] > maxgc)
+    pure_gram = not terms and r1 is None and r2 is None and Z_out is None
     zbuf = Z_out
-    if needs_multi and zbuf is None:
+    if needs_multi and zbuf is None and not pure_gram:
         zbuf = empty_block(n, p, Z_in.device if Z_in is not None else None,
                            torch.complex128 if cplx else torch.float64)
     cur_in = Z_in
@@ -395,10 +403,18 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
             continue
         if gmode == 1 and gb.shape[1] > maxgc:
             gc = gb.shape[1]
-            _tall_call(n, p, cur_in, zbuf, t1, t2, r1, r2, 1, gb[:, :maxgc], gout[:maxgc, :], cplx)
-            for g0 in range(maxgc, gc, maxgc):
-                g1 = min(gc, g0 + maxgc)
-                _tall_call(n, p, zbuf, None, None, None, None, None, 1, gb[:, g0:g1], gout[g0:g1, :], cplx)
+            if pure_gram:
+                g0 = 0  # every chunk reads the input block directly
+                zsrc = cur_in
+            else:
+                _tall_call(n, p, cur_in, zbuf, t1, t2, r1, r2, 1, gb[:, :maxgc], gout[:maxgc, :], cplx)
+                g0 = maxgc
+                zsrc = zbuf
+            step = _c_limits(p, False)[0] if cplx else maxgc
+            while g0 < gc:
+                g1 = min(gc, g0 + step)
+                _tall_call(n, p, zsrc, None, None, None, None, None, 1, gb[:, g0:g1], gout[g0:g1, :], cplx)
+                g0 = g1
         else:
             _tall_call(n, p, cur_in, zbuf if needs_multi else Z_out, t1, t2, r1, r2, gmode, gb, gout, cplx)
 

@@ -33,7 +33,7 @@ def test_spmm_c128_bitwise_vs_complex_oracle(cuda):
 
 
 @pytest.mark.parametrize("n", [1, 777, 100003])
-@pytest.mark.parametrize("p", [1, 5, 8, 16])
+@pytest.mark.parametrize("p", [1, 5, 8, 12, 16])
 def test_tall_c128(cuda, n, p):
     from paper_1604_01713_b200 import device as D
 
@@ -56,6 +56,16 @@ def test_tall_c128(cuda, n, p):
     ss = torch.zeros(p, dtype=torch.float64, device=cuda)
     D.tall(Zo, None, gram=("sumsq", ss))
     assert _rel(ss.cpu().numpy(), (np.abs(ref) ** 2).sum(axis=0)) <= 1e-12
+    # fused update + Gram against another basis (the CGS2 pass shape), wide term lists
+    for a1, gc in ((16, 40), (130, 24)):
+        X1, S1, Gb, Z = cz(n, a1), cz(a1, p), cz(n, gc), cz(n, p)
+        Zo = D.empty_block(n, p, dtype=torch.complex128)
+        out = D.small(gc, p, dtype=torch.complex128)
+        D.tall(D.to_device_block(Z), Zo, [(D.to_device_block(X1), torch.from_numpy(S1).to(cuda), -1.0)],
+               gram=("basis", D.to_device_block(Gb), out))
+        ref = Z - X1 @ S1
+        assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
+        assert _rel(out.cpu().numpy(), Gb.conj().T @ ref) <= 1e-12
     R = np.triu(cz(p, p)) + 4 * np.eye(p)
     np.fill_diagonal(R, np.abs(np.diagonal(R)))  # real positive diagonal, as from Cholesky
     Zo2 = D.empty_block(n, p, dtype=torch.complex128)
