@@ -162,8 +162,10 @@ int rg_cholqr2_f64(int64_t n, int32_t p, const double* d_x, int64_t ldx, double*
  * interleaved (re, im) doubles; ld counts complex elements.
  *   rg_spmm_csr_c128  as rg_spmm_csr_f64 (vals interleaved complex); every
  *                     partial product and sum of (a*x) is rounded separately
- *   rg_tall_c128      as rg_tall_f64 with Gout = Gb^H z / z^H z, p <= 8,
- *                     gc <= 48, mode 3 writes p real sums of |z|^2
+ *   rg_tall_c128      as rg_tall_f64 with Gout = Gb^H z / z^H z, p <= 16;
+ *                     gc <= 48 (p <= 8) or 32 (p > 8; 64 for a pure Gram),
+ *                     staged term columns <= 256 (p <= 8) or 128 (p > 8);
+ *                     mode 3 writes p real sums of |z|^2
  *   rg_chol_c128      Hermitian Cholesky G = R^H R, p <= 64
  */
 int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_end,
@@ -177,6 +179,43 @@ int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t ldzin, doubl
                  int32_t gc, double* d_gout, void* d_work, int64_t work_bytes, void* stream);
 int64_t rg_tall_c128_workspace_bytes(int64_t n, int32_t p, int32_t a1, int32_t a2, int32_t gram_mode, int32_t gc);
 int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, double cond_tol, void* stream);
+
+/*
+ * ILU(0) preconditioner (reference precond.py:33-90).
+ *   rg_wave_schedule  HOST routine (host pointers, run once per factor): the
+ *                     level schedule of the lower (upper = 0) or upper
+ *                     (upper = 1) dependency graph of a CSR pattern with
+ *                     diagonal positions diag_pos.  Writes the rows in level
+ *                     order to order[n] and chunk offsets (chunks of <= 32
+ *                     rows of one level) to chunk[rg_wave_max_chunks(n)];
+ *                     returns the chunk count (-1 on bad arguments);
+ *                     *width = the most chunks in one level (the kernels
+ *                     size their persistent grid from it).
+ *   rg_ilu0_f64       in-place IKJ ILU(0) of d_vals on the lower schedule:
+ *                     afterwards the strictly lower entries hold L (unit
+ *                     diagonal implicit) and the rest U, bitwise as
+ *                     precond.py:60-72.  *d_zero_row (caller sets INT64_MAX)
+ *                     receives the first row whose pivot is 0 (the reference
+ *                     raises ZeroPivotError there, precond.py:63-64, :71-72).
+ *   rg_sptrsv_f64     X = L^-1 B (upper = 0, lower schedule) or X = U^-1 B
+ *                     (upper = 1, upper schedule) on the combined LU pattern;
+ *                     p <= 64 columns; X may alias B (replaces
+ *                     precond.py:87-88's spsolve_triangular).
+ * Both kernels are persistent, sync-free wavefronts: lanes wait on per-row
+ * completion flags in d_work (rg_wave_workspace_bytes(n) bytes, zeroed once
+ * at allocation; each call passes a new positive epoch).
+ */
+int64_t rg_wave_workspace_bytes(int64_t n);
+int64_t rg_wave_max_chunks(int64_t n);
+int32_t rg_wave_schedule(int64_t n, const int32_t* row_ptr, const int32_t* col_idx, const int32_t* diag_pos,
+                         int32_t upper, int32_t* order, int32_t* chunk, int32_t* n_levels, int32_t* width);
+int rg_ilu0_f64(int64_t n, const int32_t* d_row_ptr, const int32_t* d_col_idx, double* d_vals,
+                const int32_t* d_diag_pos, const int32_t* d_order, const int32_t* d_chunk, int32_t nchunks,
+                int32_t width, int64_t* d_zero_row, void* d_work, int64_t work_bytes, int32_t epoch, void* stream);
+int rg_sptrsv_f64(int64_t n, const int32_t* d_row_ptr, const int32_t* d_col_idx, const double* d_vals,
+                  const int32_t* d_diag_pos, const int32_t* d_order, const int32_t* d_chunk, int32_t nchunks,
+                  int32_t width, int32_t upper, int32_t p, const double* d_b, int64_t ldb, double* d_x, int64_t ldx, void* d_work,
+                  int64_t work_bytes, int32_t epoch, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,10 @@ What it restates (reference = /root/reference/pkg/src/recgmres):
 * ``arnoldi_step``    arnoldi.py:139-193  (SpMM + CGS2 + QR; breakdown repair
                       omitted: the timed / checked inputs are full rank)
 * ``gram``/``update`` the numpy ``@`` products of arnoldi.py / solver.py
+* ``ilu0``            precond.py:33-76  (C, IKJ on the pattern, separately
+                      rounded -> bitwise equal to the reference's factors)
+* ``apply_precond``   precond.py:79-90  (textbook substitution; the reference
+                      uses SuperLU, so equal within rounding only)
 
 Parity pinning: tests/test_oracle_golden.py checks every function here
 against golden vectors produced by running the real reference package
@@ -54,6 +58,11 @@ def _load():
             fn.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                            ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
                            ctypes.c_int64, ctypes.c_int32]
+        lib.oracle_ilu0_f64.restype = ctypes.c_int64
+        lib.oracle_ilu0_f64.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 5
+        lib.oracle_trsv_f64.restype = None
+        lib.oracle_trsv_f64.argtypes = ([ctypes.c_int64] + [ctypes.c_void_p] * 4 + [ctypes.c_int32, ctypes.c_int32,
+                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64])
         _lib = lib
     return _lib
 
@@ -160,3 +169,58 @@ def arnoldi_step(row_ptr, col_idx, values, Vm, C, W, rank_tol: float = 1e-12, nt
 
 def spmm_bytes(n_rows: int, nnz: int, p: int, elem: int = 8) -> int:
     return nnz * (elem + 4) + (n_rows + 1) * 4 + 2 * p * n_rows * elem
+
+
+# ---------------------------------------------------------------------------
+# ILU(0) (precond.py)
+# ---------------------------------------------------------------------------
+
+
+class OracleZeroPivot(ArithmeticError):
+    pass
+
+
+def _diag_pos(rp, ci):
+    n = rp.shape[0] - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp))
+    hit = np.flatnonzero(ci == rows)
+    d = np.full(n, -1, dtype=np.int64)
+    d[rows[hit]] = hit
+    return d
+
+
+def ilu0(row_ptr, col_idx, values):
+    """(lu_values, diag_pos): combined L\\U values on A's pattern, as the
+    reference's ``vals`` after precond.py:60-72.  Raises OracleZeroPivot with
+    the reference's message."""
+    lib = _load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    v = np.array(values, dtype=np.float64, copy=True)
+    n = rp.shape[0] - 1
+    d = _diag_pos(rp, ci)
+    if np.any(d < 0):
+        raise OracleZeroPivot(f"row {int(np.nonzero(d < 0)[0][0])}: no stored diagonal entry")
+    scratch = np.full(max(n, 1), -1, dtype=np.int64)
+    bad = lib.oracle_ilu0_f64(n, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, d.ctypes.data, scratch.ctypes.data)
+    if bad >= 0:
+        raise OracleZeroPivot(f"row {bad}: zero pivot in ILU(0)")
+    return v, d
+
+
+def apply_precond(row_ptr, col_idx, lu_values, diag_pos, X):
+    """U^-1 (L^-1 X) on the combined pattern (textbook substitution)."""
+    lib = _load()
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    v = np.ascontiguousarray(lu_values, dtype=np.float64)
+    d = np.ascontiguousarray(diag_pos, dtype=np.int64)
+    X = np.asfortranarray(np.asarray(X, dtype=np.float64).reshape(len(X), -1))
+    n, p = X.shape
+    Z = np.zeros_like(X, order="F")
+    Y = np.zeros_like(X, order="F")
+    lib.oracle_trsv_f64(n, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, d.ctypes.data, 0, p, X.ctypes.data, n,
+                        Z.ctypes.data, n)
+    lib.oracle_trsv_f64(n, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, d.ctypes.data, 1, p, Z.ctypes.data, n,
+                        Y.ctypes.data, n)
+    return Y

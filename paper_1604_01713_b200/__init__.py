@@ -15,6 +15,7 @@ from .recycling import RecycleSpace, load_recycle_space, save_recycle_space
 from .solver import (HostOperator, SolveReport, SolverConfig, enlarge_block, solve_block_gcrodr, solve_block_gmres,
                      solve_sequence)
 from .device import NoDeviceError
+from .precond import Ilu0Factors, ZeroPivotError, apply_precond, ilu0
 
 __version__ = "0.1.0"
 
@@ -39,4 +40,8 @@ __all__ = [
     "enlarge_block",
     "HostOperator",
     "NoDeviceError",
+    "Ilu0Factors",
+    "ZeroPivotError",
+    "ilu0",
+    "apply_precond",
 ]
