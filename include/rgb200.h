@@ -186,8 +186,9 @@ int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, d
  *                     level schedule of the lower (upper = 0) or upper
  *                     (upper = 1) dependency graph of a CSR pattern with
  *                     diagonal positions diag_pos.  Writes the rows in level
- *                     order to order[n] and chunk offsets (chunks of <= 32
- *                     rows of one level) to chunk[rg_wave_max_chunks(n)];
+ *                     order to order[n] and chunk offsets (chunks of <=
+ *                     chunk_rows rows of one level, a multiple of 32) to
+ *                     chunk[rg_wave_max_chunks(n)];
  *                     returns the chunk count (-1 on bad arguments);
  *                     *width = the most chunks in one level (the kernels
  *                     size their persistent grid from it).
@@ -208,7 +209,8 @@ int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, d
 int64_t rg_wave_workspace_bytes(int64_t n);
 int64_t rg_wave_max_chunks(int64_t n);
 int32_t rg_wave_schedule(int64_t n, const int32_t* row_ptr, const int32_t* col_idx, const int32_t* diag_pos,
-                         int32_t upper, int32_t* order, int32_t* chunk, int32_t* n_levels, int32_t* width);
+                         int32_t upper, int32_t chunk_rows, int32_t* order, int32_t* chunk, int32_t* n_levels,
+                         int32_t* width);
 int rg_ilu0_f64(int64_t n, const int32_t* d_row_ptr, const int32_t* d_col_idx, double* d_vals,
                 const int32_t* d_diag_pos, const int32_t* d_order, const int32_t* d_chunk, int32_t nchunks,
                 int32_t width, int64_t* d_zero_row, void* d_work, int64_t work_bytes, int32_t epoch, void* stream);
@@ -216,6 +218,25 @@ int rg_sptrsv_f64(int64_t n, const int32_t* d_row_ptr, const int32_t* d_col_idx,
                   const int32_t* d_diag_pos, const int32_t* d_order, const int32_t* d_chunk, int32_t nchunks,
                   int32_t width, int32_t upper, int32_t p, const double* d_b, int64_t ldb, double* d_x, int64_t ldx, void* d_work,
                   int64_t work_bytes, int32_t epoch, void* stream);
+/*
+ * Level-ordered solve (used by apply_precond):
+ *   rg_wave_permute      HOST: renumber one triangle by its schedule (pos,
+ *                        permuted rp/ci, entry map); returns its entry count
+ *   rg_gather_f64        dst[j] = src[idx[j]] (permuted values, U diagonal)
+ *   rg_permute_rows_f64  move a block between the column-major original
+ *                        order (null pos) and a row-major level order
+ *   rg_sptrsv_perm_f64   in-place solve on the row-major level-ordered block;
+ *                        d_dval = U's diagonal in level order (null: unit L)
+ */
+int64_t rg_wave_permute(int64_t n, const int32_t* row_ptr, const int32_t* col_idx, const int32_t* diag_pos,
+                        int32_t upper, const int32_t* order, int32_t* pos, int32_t* rp_out, int32_t* ci_out,
+                        int64_t* emap);
+int rg_gather_f64(int64_t m, const int64_t* d_idx, const double* d_src, double* d_dst, void* stream);
+int rg_permute_rows_f64(int64_t n, int32_t p, const double* d_src, int64_t lds, const int32_t* d_pos_src,
+                        double* d_dst, int64_t ldd, const int32_t* d_pos_dst, void* stream);
+int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, const double* d_vals,
+                       const double* d_dval, const int32_t* d_chunk, int32_t nchunks, int32_t width, int32_t p,
+                       double* d_xw, void* d_work, int64_t work_bytes, int32_t epoch, void* stream);
 
 #ifdef __cplusplus
 }

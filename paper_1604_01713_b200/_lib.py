@@ -49,9 +49,14 @@ PROTOTYPES = {
     "rg_chol_c128": (ctypes.c_int, [c_i32, c_ptr, c_ptr, c_ptr, c_dbl, c_ptr]),
     "rg_wave_workspace_bytes": (c_i64, [c_i64]),
     "rg_wave_max_chunks": (c_i64, [c_i64]),
-    "rg_wave_schedule": (c_i32, [c_i64, c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "rg_wave_schedule": (c_i32, [c_i64, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr]),
     "rg_ilu0_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr,
                                    c_i64, c_i32, c_ptr]),
+    "rg_wave_permute": (c_i64, [c_i64, c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "rg_gather_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "rg_permute_rows_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
+    "rg_sptrsv_perm_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_i32, c_ptr,
+                                          c_ptr, c_i64, c_i32, c_ptr]),
     "rg_sptrsv_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i32,
                                      c_ptr,
                                      c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr]),

@@ -7,7 +7,8 @@
 // forward solve; the upper part (rows k > i) orders the backward solve.
 // rg_wave_schedule (host code, once per factorisation) assigns every row
 // its level (1 + the deepest level it reads) and lists the rows level by
-// level in chunks of at most 32 rows of ONE level.  Kernels are persistent
+// level in chunks of up to chunk_rows rows (a multiple of 32) of ONE level;
+// a lane takes every 32nd row of its warp's chunk.  Kernels are persistent
 // and sync-free: a warp claims the next chunk from a global ticket, each
 // lane takes one row, polls (relaxed loads, then one acquire fence) the
 // completion flag of every row it reads, computes, and publishes its row
@@ -82,9 +83,9 @@ __global__ void __launch_bounds__(kWaveWarps * 32) ilu0_kernel(Wave W, const int
   for (;;) {
     const int32_t c = claim_chunk(W.ticket, lane);
     if (c >= W.nchunks) return;
-    const int32_t e0 = W.chunk[c], e1 = W.chunk[c + 1];
-    if (e0 + lane >= e1) continue;
-    const int32_t i = W.order[e0 + lane];
+    const int32_t e1 = W.chunk[c + 1];
+    for (int32_t ee_ = W.chunk[c] + lane; ee_ < e1; ee_ += 32) {
+    const int32_t i = W.order[ee_];
     const int32_t lo = rp[i], hi = rp[i + 1], di = dpos[i];
     for (int32_t t = lo; t < di; ++t) wait_row(W.flags, ci[t], W.epoch, W.ns_max);
     fence_acquire();
@@ -106,6 +107,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) ilu0_kernel(Wave W, const int
     }
     if (vals[di] == 0.0) atomicMin(zero_row, (long long)i);
     st_release(W.flags + i, W.epoch);
+    }
   }
 }
 
@@ -120,9 +122,9 @@ __global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_kernel(Wave W, const i
   for (;;) {
     const int32_t c = claim_chunk(W.ticket, lane);
     if (c >= W.nchunks) return;
-    const int32_t e0 = W.chunk[c], e1 = W.chunk[c + 1];
-    if (e0 + lane >= e1) continue;
-    const int32_t i = W.order[e0 + lane];
+    const int32_t e1 = W.chunk[c + 1];
+    for (int32_t ee_ = W.chunk[c] + lane; ee_ < e1; ee_ += 32) {
+    const int32_t i = W.order[ee_];
     const int32_t di = dpos[i];
     const int32_t eb = UPPER ? di + 1 : rp[i];
     const int32_t ee = UPPER ? rp[i + 1] : di;
@@ -145,7 +147,77 @@ __global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_kernel(Wave W, const i
         if (c0 + q < p) X[i + (int64_t)(c0 + q) * ldx] = UPPER ? __ddiv_rn(acc[q], dinv_src) : acc[q];
     }
     st_release(W.flags + i, W.epoch);
+    }
   }
+}
+
+// Level-ordered variant of the solve.  The triangle is renumbered by its
+// schedule (row r of the permuted matrix = the r-th row in level order,
+// columns renamed to level positions, entries kept in their original order)
+// and the block lives in a row-major workspace in the same order, so the 32
+// lanes of a chunk read 32 consecutive CSR rows and 32 consecutive block rows
+// (p contiguous doubles each) instead of rows a grid-line apart.  Arithmetic
+// is the same as sptrsv_kernel's.
+__global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_perm_kernel(Wave W, const int32_t* __restrict__ rp,
+                                                                       const int32_t* __restrict__ ci,
+                                                                       const double* __restrict__ vals,
+                                                                       const double* __restrict__ dval, int p,
+                                                                       double* Xw) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    const int32_t c = claim_chunk(W.ticket, lane);
+    if (c >= W.nchunks) return;
+    const int32_t ce = W.chunk[c + 1];
+    // all rows of this lane (same level) first wait, then one acquire fence
+    for (int32_t r = W.chunk[c] + lane; r < ce; r += 32)
+      for (int32_t e = rp[r]; e < rp[r + 1]; ++e) wait_row(W.flags, ci[e], W.epoch, W.ns_max);
+    fence_acquire();
+    for (int32_t r = W.chunk[c] + lane; r < ce; r += 32) {
+    const int32_t eb = rp[r], ee = rp[r + 1];
+    double* xr = Xw + (int64_t)r * p;
+    for (int c0 = 0; c0 < p; c0 += 8) {
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = (c0 + q < p) ? xr[c0 + q] : 0.0;
+      for (int32_t e = eb; e < ee; ++e) {
+        const double v = vals[e];
+        const double* xk = Xw + (int64_t)ci[e] * p + c0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (c0 + q < p) acc[q] = __dsub_rn(acc[q], __dmul_rn(v, __ldcg(xk + q)));
+      }
+      if (dval) {
+        const double d = dval[r];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = __ddiv_rn(acc[q], d);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q < p) xr[c0 + q] = acc[q];
+    }
+    st_release(W.flags + r, W.epoch);
+    }
+  }
+}
+
+// dst row pos_d[i] <- src row pos_s[i]; a null position array means the
+// column-major layout in original order (leading dimension ld), otherwise a
+// row-major p-wide layout in the permuted order.
+__global__ void permute_rows_kernel(int64_t n, int p, const double* __restrict__ src, int64_t lds,
+                                    const int32_t* __restrict__ pos_s, double* __restrict__ dst, int64_t ldd,
+                                    const int32_t* __restrict__ pos_d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double* sr = pos_s ? src + (int64_t)pos_s[i] * p : src + i;
+    double* dr = pos_d ? dst + (int64_t)pos_d[i] * p : dst + i;
+    const int64_t ss = pos_s ? 1 : lds, ds = pos_d ? 1 : ldd;
+    for (int c = 0; c < p; ++c) dr[c * ds] = sr[c * ss];
+  }
+}
+
+__global__ void gather_kernel(int64_t m, const int64_t* __restrict__ idx, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m; j += (int64_t)gridDim.x * blockDim.x)
+    dst[j] = src[idx[j]];
 }
 
 static int64_t wave_grid(int32_t nchunks, int32_t width) {
@@ -166,14 +238,15 @@ extern "C" int64_t rg_wave_workspace_bytes(int64_t n) { return 256 + 4 * (n > 0 
 
 // Host-side schedule (runs on the CPU once per factorisation; no numerics).
 extern "C" int32_t rg_wave_schedule(int64_t n, const int32_t* row_ptr, const int32_t* col_idx,
-                                    const int32_t* diag_pos, int32_t upper, int32_t* order, int32_t* chunk,
-                                    int32_t* n_levels, int32_t* width) {
+                                    const int32_t* diag_pos, int32_t upper, int32_t chunk_rows, int32_t* order,
+                                    int32_t* chunk, int32_t* n_levels, int32_t* width) {
   using namespace rg;
   clear_error();
   if (n < 0 || (n > 0 && (!row_ptr || !col_idx || !diag_pos || !order || !chunk))) {
     set_error("rg_wave_schedule: bad arguments");
     return -1;
   }
+  const int32_t cr = chunk_rows >= 32 ? (chunk_rows / 32) * 32 : 32;  // rows per chunk, a multiple of 32
   std::vector<int32_t> lev((size_t)n, 0);
   int32_t maxlev = 0;
   for (int64_t r = 0; r < n; ++r) {
@@ -198,8 +271,8 @@ extern "C" int32_t rg_wave_schedule(int64_t n, const int32_t* row_ptr, const int
   chunk[0] = 0;
   for (int32_t l = 0; l < nl; ++l) {
     const int32_t c0 = nc;
-    for (int64_t s = start[(size_t)l]; s < start[(size_t)l + 1]; s += 32)
-      chunk[++nc] = (int32_t)std::min<int64_t>(s + 32, start[(size_t)l + 1]);
+    for (int64_t s = start[(size_t)l]; s < start[(size_t)l + 1]; s += cr)
+      chunk[++nc] = (int32_t)std::min<int64_t>(s + cr, start[(size_t)l + 1]);
     wmax = std::max(wmax, nc - c0);
   }
   if (n_levels) *n_levels = nl;
@@ -207,7 +280,7 @@ extern "C" int32_t rg_wave_schedule(int64_t n, const int32_t* row_ptr, const int
   return nc;
 }
 
-extern "C" int64_t rg_wave_max_chunks(int64_t n) { return n / 32 + n + 2; }
+extern "C" int64_t rg_wave_max_chunks(int64_t n) { return n / 32 + n + 2; }  // any chunk_rows >= 32
 
 static rg::Wave make_wave(const int32_t* order, const int32_t* chunk, int32_t nchunks, void* d_work, int32_t epoch) {
   rg::Wave W;
@@ -268,5 +341,75 @@ extern "C" int rg_sptrsv_f64(int64_t n, const int32_t* d_row_ptr, const int32_t*
     sptrsv_kernel<false><<<g, kWaveWarps * 32, 0, s>>>(W, d_row_ptr, d_col_idx, d_vals, d_diag_pos, p, d_b, ldb,
                                                        d_x, ldx);
   RG_CHECK_LAUNCH("rg_sptrsv_f64");
+  return RG_OK;
+}
+
+// Host: the schedule-ordered copy of one triangle's pattern.  pos[i] = level
+// position of row i; rp_out/ci_out = the permuted strictly-lower (upper = 0)
+// or strictly-upper (upper = 1) pattern; emap[e'] = original entry index of
+// permuted entry e' (values are gathered on the device after factorising).
+// Returns the triangle's entry count.
+extern "C" int64_t rg_wave_permute(int64_t n, const int32_t* row_ptr, const int32_t* col_idx, const int32_t* diag_pos,
+                                   int32_t upper, const int32_t* order, int32_t* pos, int32_t* rp_out, int32_t* ci_out,
+                                   int64_t* emap) {
+  for (int64_t r = 0; r < n; ++r) pos[order[r]] = (int32_t)r;
+  int64_t m = 0;
+  rp_out[0] = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t i = order[r];
+    const int32_t eb = upper ? diag_pos[i] + 1 : row_ptr[i];
+    const int32_t ee = upper ? row_ptr[i + 1] : diag_pos[i];
+    for (int32_t e = eb; e < ee; ++e) {
+      ci_out[m] = pos[col_idx[e]];
+      emap[m] = e;
+      ++m;
+    }
+    rp_out[r + 1] = (int32_t)m;
+  }
+  return m;
+}
+
+extern "C" int rg_gather_f64(int64_t m, const int64_t* d_idx, const double* d_src, double* d_dst, void* stream) {
+  using namespace rg;
+  clear_error();
+  if (m <= 0) return RG_OK;
+  RG_REQUIRE(d_idx && d_src && d_dst, "rg_gather_f64: null argument");
+  const int64_t g = std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 16);
+  gather_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(m, d_idx, d_src, d_dst);
+  RG_CHECK_LAUNCH("rg_gather_f64");
+  return RG_OK;
+}
+
+extern "C" int rg_permute_rows_f64(int64_t n, int32_t p, const double* d_src, int64_t lds, const int32_t* d_pos_src,
+                                   double* d_dst, int64_t ldd, const int32_t* d_pos_dst, void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n >= 0 && p >= 1, "rg_permute_rows_f64: bad shape");
+  if (n == 0) return RG_OK;
+  RG_REQUIRE(d_src && d_dst && (d_pos_src || lds >= n) && (d_pos_dst || ldd >= n), "rg_permute_rows_f64: bad args");
+  const int64_t g = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
+  permute_rows_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(n, p, d_src, lds, d_pos_src, d_dst, ldd,
+                                                                     d_pos_dst);
+  RG_CHECK_LAUNCH("rg_permute_rows_f64");
+  return RG_OK;
+}
+
+extern "C" int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, const double* d_vals,
+                                  const double* d_dval, const int32_t* d_chunk, int32_t nchunks, int32_t width,
+                                  int32_t p, double* d_xw, void* d_work, int64_t work_bytes, int32_t epoch,
+                                  void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n >= 0 && n < (1ll << 31) && p >= 1, "rg_sptrsv_perm_f64: n=%lld p=%d", (long long)n, p);
+  if (n == 0) return RG_OK;
+  RG_REQUIRE(d_rp && d_ci && d_chunk && d_xw, "rg_sptrsv_perm_f64: null argument");
+  RG_REQUIRE(d_work && work_bytes >= rg_wave_workspace_bytes(n), "rg_sptrsv_perm_f64: workspace too small");
+  RG_REQUIRE(epoch > 0, "rg_sptrsv_perm_f64: epoch must be positive");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaMemsetAsync(d_work, 0, 4, s);
+  Wave W = make_wave(nullptr, d_chunk, nchunks, d_work, epoch);
+  sptrsv_perm_kernel<<<(unsigned)wave_grid(nchunks, width), kWaveWarps * 32, 0, s>>>(W, d_rp, d_ci, d_vals, d_dval,
+                                                                                     p, d_xw);
+  RG_CHECK_LAUNCH("rg_sptrsv_perm_f64");
   return RG_OK;
 }

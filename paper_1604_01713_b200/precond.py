@@ -25,6 +25,8 @@ device layout on first use.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -38,6 +40,10 @@ class ZeroPivotError(ArithmeticError):
 
 
 _INT64_MAX = np.iinfo(np.int64).max
+# RG_ILU_PERM=0 solves in the original row order (the A/B baseline of tools/prof_ilu.py)
+_PERM = os.environ.get("RG_ILU_PERM", "1") != "0"
+# rows per wavefront chunk (each lane of a warp takes chunk_rows / 32 rows of one level)
+_CHUNK_ROWS = int(os.environ.get("RG_WAVE_CHUNK", "32"))
 
 
 class _Schedule:
@@ -51,14 +57,44 @@ class _Schedule:
         nl = np.zeros(1, dtype=np.int32)
         wd = np.zeros(1, dtype=np.int32)
         nc = L.rg_wave_schedule(n, rp_h.ctypes.data, ci_h.ctypes.data, dpos_h.ctypes.data, 1 if upper else 0,
-                                order.ctypes.data, chunk.ctypes.data, nl.ctypes.data, wd.ctypes.data)
+                                _CHUNK_ROWS, order.ctypes.data, chunk.ctypes.data, nl.ctypes.data, wd.ctypes.data)
         if nc < 0:
             raise ValueError("rg_wave_schedule failed")
         self.nchunks = int(nc)
         self.levels = int(nl[0])
         self.width = int(wd[0])
+        self.upper = upper
+        self.order_h = order[:n]
         self.order = torch.from_numpy(order).to(device)
         self.chunk = torch.from_numpy(chunk[: nc + 1].copy()).to(device)
+        self.perm = None
+
+    def build_perm(self, rp_h, ci_h, dpos_h, lu_vals: torch.Tensor):
+        """Level-ordered copy of this triangle (rg_wave_permute) with its
+        values gathered from the factor on the device."""
+        L = _dev.lib()
+        n = len(rp_h) - 1
+        dev = lu_vals.device
+        nnz = len(ci_h)
+        pos = np.empty(max(n, 1), dtype=np.int32)
+        rp_o = np.empty(n + 1, dtype=np.int32)
+        ci_o = np.empty(max(nnz, 1), dtype=np.int32)
+        emap = np.empty(max(nnz, 1), dtype=np.int64)
+        m = int(L.rg_wave_permute(n, rp_h.ctypes.data, ci_h.ctypes.data, dpos_h.ctypes.data, 1 if self.upper else 0,
+                                  self.order_h.ctypes.data, pos.ctypes.data, rp_o.ctypes.data, ci_o.ctypes.data,
+                                  emap.ctypes.data))
+        d_emap = torch.from_numpy(emap[:max(m, 1)].copy()).to(dev)
+        vals = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+        _lib.check(L.rg_gather_f64(m, d_emap.data_ptr(), lu_vals.data_ptr(), vals.data_ptr(), _dev.stream_ptr()),
+                   "gather")
+        dval = None
+        if self.upper:
+            didx = torch.from_numpy(dpos_h[self.order_h].astype(np.int64)).to(dev)
+            dval = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+            _lib.check(L.rg_gather_f64(n, didx.data_ptr(), lu_vals.data_ptr(), dval.data_ptr(), _dev.stream_ptr()),
+                       "gather")
+        self.perm = dict(pos=torch.from_numpy(pos).to(dev), rp=torch.from_numpy(rp_o).to(dev),
+                         ci=torch.from_numpy(ci_o[:max(m, 1)].copy()).to(dev), vals=vals, dval=dval)
 
 
 class _DeviceLu:
@@ -78,6 +114,8 @@ class _DeviceLu:
         self.dpos = torch.from_numpy(dpos_h).to(device)
         self.lower_sched = _Schedule(rp_h, ci_h, dpos_h, False, device)
         self.upper_sched = _Schedule(rp_h, ci_h, dpos_h, True, device)
+        self._host_pattern = (rp_h, ci_h, dpos_h)
+        self._ws = {}
         L = _dev.lib()
         self.work = torch.zeros(int(L.rg_wave_workspace_bytes(n)), dtype=torch.uint8, device=device)
         self.epoch = 0
@@ -99,6 +137,47 @@ class _DeviceLu:
                            _dev.stream_ptr())
         _lib.check(rc, "ilu0")
         _dev.LaunchLog.count += 1
+
+    def _permuted(self):
+        if self.lower_sched.perm is None:
+            rp_h, ci_h, dpos_h = self._host_pattern
+            self.lower_sched.build_perm(rp_h, ci_h, dpos_h, self.vals)
+            self.upper_sched.build_perm(rp_h, ci_h, dpos_h, self.vals)
+        return self.lower_sched, self.upper_sched
+
+    def apply(self, B: torch.Tensor, out: torch.Tensor) -> None:
+        """out = U^-1 (L^-1 B) through the level-ordered row-major layout:
+        scatter B into L's order, solve, re-order into U's, solve, gather back."""
+        L = _dev.lib()
+        n, p = B.shape
+        ls, us = self._permuted()
+        key = p
+        if key not in self._ws:
+            self._ws[key] = (torch.empty(max(n * p, 1), dtype=torch.float64, device=self.device),
+                             torch.empty(max(n * p, 1), dtype=torch.float64, device=self.device))
+        w1, w2 = self._ws[key]
+        st = _dev.stream_ptr()
+        lp, up = ls.perm, us.perm
+
+        def perm(src, lds, ps, dst, ldd, pd):
+            _lib.check(L.rg_permute_rows_f64(n, p, src.data_ptr(), lds, ps.data_ptr() if ps is not None else None,
+                                             dst.data_ptr(), ldd, pd.data_ptr() if pd is not None else None, st),
+                       "permute_rows")
+            _dev.LaunchLog.count += 1
+
+        def solve(sc, pm, w):
+            rc = L.rg_sptrsv_perm_f64(n, pm["rp"].data_ptr(), pm["ci"].data_ptr(), pm["vals"].data_ptr(),
+                                      pm["dval"].data_ptr() if pm["dval"] is not None else None,
+                                      sc.chunk.data_ptr(), sc.nchunks, sc.width, p, w.data_ptr(),
+                                      self.work.data_ptr(), self.work.numel(), self.next_epoch(), st)
+            _lib.check(rc, "sptrsv_perm")
+            _dev.LaunchLog.count += 1
+
+        perm(B, _dev.ld_of(B), None, w1, 0, lp["pos"])
+        solve(ls, lp, w1)
+        perm(w1, 0, lp["pos"], w2, 0, up["pos"])
+        solve(us, up, w2)
+        perm(w2, 0, up["pos"], out, _dev.ld_of(out), None)
 
     def solve(self, B: torch.Tensor, X: torch.Tensor, upper: bool) -> None:
         L = _dev.lib()
@@ -240,8 +319,11 @@ def apply_precond_device(F: Ilu0Factors, X: torch.Tensor, out: torch.Tensor | No
         out = _dev.empty_block(X.shape[0], X.shape[1], X.device, X.dtype)
     if X.shape[1] == 0 or F.n == 0:
         return out
-    lu.solve(X, out, upper=False)
-    lu.solve(out, out, upper=True)
+    if _PERM:
+        lu.apply(X, out)
+    else:
+        lu.solve(X, out, upper=False)
+        lu.solve(out, out, upper=True)
     return out
 
 

@@ -127,3 +127,20 @@ def test_reference_precond_properties(cuda):
     # factors given as host CsrMatrix objects (the reference constructor)
     G = Ilu0Factors(lower=F.lower, upper=F.upper)
     assert np.allclose(apply_precond(G, T @ Xr), Xr, atol=1e-12)
+
+
+def test_level_ordered_solve_matches_original_order(cuda):
+    """The permuted row-major wavefront (apply) and the original-order one
+    (solve x2) do the same arithmetic: bitwise equal."""
+    from paper_1604_01713_b200 import device as D, problems
+    from paper_1604_01713_b200.precond import ilu0
+
+    A = problems.conv_diff_3d(24, 20.0)
+    lu = ilu0(A).device_lu()
+    X = D.to_device_block(np.random.default_rng(3).standard_normal((A.n_rows, 11)))
+    Y1 = D.empty_block(A.n_rows, 11)
+    lu.apply(X, Y1)
+    Y2 = D.empty_block(A.n_rows, 11)
+    lu.solve(X, Y2, upper=False)
+    lu.solve(Y2, Y2, upper=True)
+    assert torch.equal(Y1, Y2)
