@@ -8,11 +8,13 @@ computing on the host.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 import threading
 
 _PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "librgb200.so"
+# RG_LIB_PATH selects an alternative build of the same library (tools/ab_build.py variants)
+LIB_PATH = pathlib.Path(os.environ["RG_LIB_PATH"]) if os.environ.get("RG_LIB_PATH") else _PKG / "_lib" / "librgb200.so"
 
 RG_OK, RG_EBADARG, RG_ECUDA = 0, 1, 2
 

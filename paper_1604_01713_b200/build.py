@@ -45,13 +45,16 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    """Compile every .cu into librgb200.so (objects in parallel, then link)."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
+          extra_flags: list[str] | None = None) -> pathlib.Path:
+    """Compile every .cu into librgb200.so (objects in parallel, then link).
+    ``out`` / ``extra_flags`` build a variant library (A/B experiments)."""
+    target = LIB_PATH if out is None else pathlib.Path(out)
+    if out is None and not force and not _stale():
         return LIB_PATH
     LIB_DIR.mkdir(exist_ok=True)
     nvcc = _nvcc()
-    objdir = LIB_DIR / "obj"
+    objdir = LIB_DIR / ("obj" if out is None else "obj_" + target.stem)
     objdir.mkdir(exist_ok=True)
     procs = []
     objs = []
@@ -61,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
             continue
         obj = objdir / (path.stem + ".o")
         objs.append(obj)
-        cmd = [nvcc, *NVCC_FLAGS, "-c", str(path), "-o", str(obj)]
+        cmd = [nvcc, *NVCC_FLAGS, *(extra_flags or []), "-c", str(path), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -75,11 +78,12 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
     if failed:
         msg = "\n".join(f"--- {s}\n{o}" for s, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    target.parent.mkdir(parents=True, exist_ok=True)
+    tmp = target.with_suffix(".so.tmp")
     subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
                     *map(str, objs)], check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

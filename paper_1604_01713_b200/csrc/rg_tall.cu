@@ -853,16 +853,27 @@ struct SlabPlan {
   int nz, n1, n2, ng, total;
 };
 
-constexpr int kV6Warps = 8;
+#ifndef RG_V6_CA
+#define RG_V6_CA 0
+#endif
+constexpr bool kCaCopy = RG_V6_CA != 0;
+
+#ifndef RG_V6_WARPS
+#define RG_V6_WARPS 8
+#endif
+#ifndef RG_V6_RING
+#define RG_V6_RING 4
+#endif
+constexpr int kV6Warps = RG_V6_WARPS;
 constexpr int kV6Threads = kV6Warps * 32;
-constexpr int kRing6 = 4;
+constexpr int kRing6 = RG_V6_RING;
 constexpr int kSS6 = 36;
 constexpr int kMaxSlabs = 96;
 
 struct SlabTab {
-  const double* ptr[kMaxSlabs];
-  int64_t ld[kMaxSlabs];
-  int nc[kMaxSlabs];
+  const double* ptr[kMaxSlabs][2];  // slab base for lanes of column parity 0 / 1
+  int64_t ld2[kMaxSlabs];           // 2 * leading dimension (a lane's next chunk)
+  int nv[kMaxSlabs][2];             // valid 16-byte chunks per column parity (0..4)
 };
 
 template <int PM, int MTMAX>
@@ -913,9 +924,13 @@ __global__ void __launch_bounds__(kV6Threads, 2) tall_v6_kernel(TallParams P, Sl
       ptr = P.gb; ld = P.ldgb; nc = P.gc - (k - L.nz - L.n1 - L.n2) * 8;
     }
     const int s = k < L.nz ? k : (k < L.nz + L.n1 ? k - L.nz : (k < L.nz + L.n1 + L.n2 ? k - L.nz - L.n1 : k - L.nz - L.n1 - L.n2));
-    tab.ptr[k] = ptr + (int64_t)(s * 8) * ld;
-    tab.ld[k] = ld;
-    tab.nc[k] = nc > 8 ? 8 : nc;
+    const double* b = ptr + (int64_t)(s * 8) * ld;
+    const int ncc = nc > 8 ? 8 : nc;
+    tab.ptr[k][0] = b;
+    tab.ptr[k][1] = b + ld;
+    tab.ld2[k] = 2 * ld;
+    tab.nv[k][0] = (ncc + 1) >> 1;  // columns 0, 2, 4, 6 below ncc
+    tab.nv[k][1] = ncc >> 1;        // columns 1, 3, 5, 7 below ncc
   }
   __syncthreads();
 
@@ -943,32 +958,56 @@ __global__ void __launch_bounds__(kV6Threads, 2) tall_v6_kernel(TallParams P, Sl
   // per-lane chunk geometry: chunk t covers column (lane>>4) + 2t, rows 2*(lane&15) .. +1
   const int ccol = lane >> 4, rp2 = 2 * (lane & 15);
   int64_t iss_left = my_units * L.total;
-  int64_t iss_r0 = gwarp * 32;
-  int iss_k = 0, iss_slot = 0;
+  int64_t iss_row = gwarp * 32 + rp2;  // this lane's first row of the unit being issued
+  int iss_k = 0;
+  // shared-memory destination of this lane's chunk t in slot q:
+  //   dst_lane + q * 8 * kSS6 + 2 * t * kSS6   (column ccol + 2t, rows rp2, rp2 + 1)
+  const uint32_t dst_lane =
+      static_cast<uint32_t>(__cvta_generic_to_shared(ring + ccol * kSS6 + rp2));
+  uint32_t dst_slot = dst_lane;
+  const uint32_t dst_wrap = dst_lane + kRing6 * 8 * kSS6 * 8;
+  auto row_bytes = [&](int64_t row) {
+    const int64_t vr = P.n - row;
+    return vr >= 2 ? 16 : (vr == 1 ? 8 : 0);
+  };
+  int rowbytes = row_bytes(iss_row);
   auto issue_next = [&]() {
     if (iss_left > 0) {
-      const double* base = tab.ptr[iss_k];
-      const int64_t ld = tab.ld[iss_k];
-      const int nc = tab.nc[iss_k];
-      int64_t vr = P.n - (iss_r0 + rp2);
-      vr = vr < 0 ? 0 : (vr > 2 ? 2 : vr);
-      const int rowbytes = (int)vr * 8;
-      const double* src0 = base + iss_r0 + rp2;
-      double* dst0 = ring + iss_slot * 8 * kSS6 + rp2;
+      const double* src = tab.ptr[iss_k][ccol] + iss_row;
+      const int64_t ld2 = tab.ld2[iss_k];
+      const int nv = tab.nv[iss_k][ccol];
+      if (rowbytes == 16 && kCaCopy) {
+        // .ca: the two 16-byte halves of a sector that two lanes request are
+        // served by one L2 read (the .cg form fetches the sector twice)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int c = ccol + 2 * t;
-        const int bytes = c < nc ? rowbytes : 0;
-        cp_async16(dst0 + c * kSS6, bytes ? src0 + (int64_t)c * ld : base, bytes);
+        for (int t = 0; t < 4; ++t) {
+          asm volatile(
+              "{\n .reg .pred q;\n setp.ge.s32 q, %2, %3;\n"
+              " cp.async.ca.shared.global [%0], [%1], 16, q;\n}\n" ::"r"(dst_slot + t * 2 * kSS6 * 8),
+              "l"(t < nv ? src : tab.ptr[0][0]), "r"(t), "r"(nv)
+              : "memory");
+          src += ld2;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int bytes = t < nv ? rowbytes : 0;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst_slot + t * 2 * kSS6 * 8),
+                       "l"(bytes ? src : tab.ptr[0][0]), "r"(bytes)
+                       : "memory");
+          src += ld2;
+        }
       }
       --iss_left;
       if (++iss_k == L.total) {
         iss_k = 0;
-        iss_r0 += nwarps * 32;
+        iss_row += nwarps * 32;
+        rowbytes = row_bytes(iss_row);
       }
     }
     cp_async_commit();
-    if (++iss_slot == kRing6) iss_slot = 0;
+    dst_slot += 8 * kSS6 * 8;
+    if (dst_slot == dst_wrap) dst_slot = dst_lane;
   };
 #pragma unroll
   for (int s = 0; s < kRing6; ++s) issue_next();
