@@ -253,7 +253,7 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     Vnew = fact.v_block(m + 1)
 
     if ortho == "cgs2":
-        if _dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P and fact.k + (m + 1) * L <= 256:
+        if _dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED and fact.k + (m + 1) * L <= 256:
             # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64)
             _dev.cgs2(Ahat, C, active, fact._coef, scr.G1)
         else:

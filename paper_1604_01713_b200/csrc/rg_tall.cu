@@ -795,7 +795,9 @@ static int pick_pm(int p) {
   if (p <= 2) return 2;
   if (p <= 4) return 4;
   if (p <= 8) return 8;
-  return 16;
+  if (p <= 16) return 16;
+  if (p <= 24) return 24;  // wide blocks (recycle space k = 20): v6 only
+  return 32;
 }
 static int pick_mtmax(int mtiles) {
   if (mtiles <= 2) return 2;
@@ -877,7 +879,7 @@ struct SlabTab {
 };
 
 template <int PM, int MTMAX>
-__global__ void __launch_bounds__(kV6Threads, 2) tall_v6_kernel(TallParams P, SlabPlan L) {
+__global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(TallParams P, SlabPlan L) {
   constexpr int PM8 = PM < 8 ? 8 : PM;
   constexpr int NT = PM8 / 8;
   constexpr int MTA = MTMAX > 0 ? MTMAX : 1;
@@ -1224,7 +1226,7 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
                        (size_t)std::max(MTMAX * NT * 64, kV6Warps * PM)) * sizeof(double);
   static int per_sm = -1;
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     int v = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kV6Threads, smem);
     per_sm = v < 1 ? 1 : v;
@@ -1361,7 +1363,9 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   using namespace rg;
   clear_error();
   RG_REQUIRE(n >= 0, "rg_tall_f64: n=%lld < 0", (long long)n);
-  RG_REQUIRE(p >= 1 && p <= 16, "rg_tall_f64: block width p=%d outside [1, 16]", p);
+  RG_REQUIRE(p >= 1 && p <= 32, "rg_tall_f64: block width p=%d outside [1, 32]", p);
+  RG_REQUIRE(p <= 16 || gram_mode == 0 || gram_mode == 3 || gc <= (p <= 24 ? 32 : 16),
+             "rg_tall_f64: Gram basis width gc=%d too wide for p=%d (32 for p <= 24, 16 above)", gc, p);
   RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= 512, "rg_tall_f64: term widths %d, %d", a1, a2);
   RG_REQUIRE(!d_zin || ldzin >= n, "rg_tall_f64: ldzin < n");
   RG_REQUIRE(!d_zout || ldzout >= n, "rg_tall_f64: ldzout < n");
@@ -1396,8 +1400,28 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const int64_t bound = tall_grid_bound();
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
-  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512 && aligned16(P.zin, P.ldzin) &&
-      aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) && (gram_mode != 1 || aligned16(P.gb, P.ldgb)) ) {
+  const bool aligned = aligned16(P.zin, P.ldzin) && aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) &&
+                       (gram_mode != 1 || aligned16(P.gb, P.ldgb));
+  if (p > 16) {
+    // wide blocks run on v6 only
+    const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
+                           (gram_mode == 1 ? (gc + 7) / 8 : 0);
+    RG_REQUIRE(aligned && ncol_slabs <= kMaxSlabs && (P.a1 + P.a2) <= 128,
+               "rg_tall_f64: p=%d > 16 needs 16-byte aligned operands, <= 128 term columns, <= %d slabs", p,
+               kMaxSlabs);
+    const int mtw = P.mtiles == 0 ? 0 : (P.mtiles <= 2 ? 2 : 4);
+    if (PM == 24)
+      e = mtw == 0 ? launch_v6<24, 0>(P, bound, st) : (mtw == 2 ? launch_v6<24, 2>(P, bound, st)
+                                                                  : launch_v6<24, 4>(P, bound, st));
+    else
+      e = mtw == 0 ? launch_v6<32, 0>(P, bound, st) : launch_v6<32, 2>(P, bound, st);
+    if (e != cudaSuccess) {
+      set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+      return RG_ECUDA;
+    }
+    return RG_OK;
+  }
+  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512 && aligned) {
     const char* impl = getenv("RG_TALL_IMPL");
     const int mt5 = (gram_mode == 1 || gram_mode == 2) ? mtmax : 0;
     // default v6 (all operands through the cp.async ring, DMMA update);

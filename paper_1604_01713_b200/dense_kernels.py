@@ -107,7 +107,7 @@ def cholqr2_launch(X: torch.Tensor, Q: torch.Tensor, scr: QrScratch, g1_ready: b
     """Enqueue CholQR2 of X into Q (Q may not alias X: X is kept intact for
     the TSQR fallback).  If ``g1_ready``, scr.G1 already holds X^T X (fused
     into the producing pass)."""
-    if _dev.fused_ok() and X.shape[1] <= _dev.MAX_P and X.dtype == torch.float64:
+    if _dev.fused_ok() and X.shape[1] <= _dev.MAX_P_FUSED and X.dtype == torch.float64:
         # G1 | R1 | G2 | R2 are the first four blocks of scr.buf, as rg_cholqr2_f64 expects
         _dev.cholqr2(X, Q, scr.buf, scr.status, g1_ready)
         return

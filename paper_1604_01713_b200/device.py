@@ -18,8 +18,16 @@ import torch
 from . import _lib
 
 LD_ALIGN = 32
-MAX_P = 16        # block width one rg_tall launch handles
-MAX_GC = 128      # Gram basis columns per launch
+MAX_P = 32        # block width one rg_tall launch handles (p > 16: v6 kernel only)
+MAX_P_FUSED = 16  # widest block of the rg_cgs2_f64 / rg_cholqr2_f64 orchestrators
+MAX_GC = 128      # Gram basis columns per launch (p <= 16)
+
+
+def _r_limits(p: int):
+    """(max Gram basis columns, max staged term columns) of one real launch."""
+    if p <= 16:
+        return MAX_GC, MAX_TERM_COLS
+    return (32 if p <= 24 else 16), 128
 MAX_TERM_COLS = 512
 MAX_P_C = 16      # complex128 limits (rg_tall_c128); blocks wider than 8 allow
 MAX_GC_C = 48     # a 32-column Gram basis and 128 staged term columns per launch
@@ -356,8 +364,8 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         _zero_gram(gram)
         return
     cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
-    maxp, maxgc = (MAX_P_C, _c_limits(p, bool(terms))[0]) if cplx else (MAX_P, MAX_GC)
-    tcols = _c_limits(p)[1] if cplx else MAX_TERM_COLS
+    maxp, maxgc = (MAX_P_C, _c_limits(p, bool(terms))[0]) if cplx else (MAX_P, _r_limits(p)[0])
+    tcols = _c_limits(p)[1] if cplx else _r_limits(p)[1]
     terms = _split_terms(terms, tcols)
     r1 = _coef(r1) if r1 is not None else None
     r2 = _coef(r2) if r2 is not None else None
