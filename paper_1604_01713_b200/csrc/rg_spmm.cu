@@ -143,11 +143,12 @@ struct UnitRp {
   int32_t wbeg, wend, mybeg, myend;
 };
 
+template <int RPW = 32>
 __device__ __forceinline__ UnitRp load_unit_rp(const int32_t* __restrict__ rp, int64_t wrow0, int64_t row_end,
                                                int lane) {
   UnitRp u;
-  const int64_t wlast = min(wrow0 + 32, row_end);
-  const int64_t i = wrow0 + lane;
+  const int64_t wlast = min(wrow0 + RPW, row_end);
+  const int64_t i = wrow0 + lane % RPW;
   u.wbeg = __ldg(rp + wrow0);
   u.wend = __ldg(rp + wlast);
   u.mybeg = i < row_end ? __ldg(rp + i) : 0;
@@ -190,29 +191,41 @@ __device__ __forceinline__ void accumulate_rows(const int32_t* sci, const double
   }
 }
 
-template <int PB>
+// CTAs per SM the register budget is sized for: 3 (85 registers) spills at
+// PB >= 6, and the spill traffic costs more than the extra warps buy
+// (cfg4 p = 8: 912 us with 3, 824 us with 2; profiles/spmm_r01.txt)
+#ifndef RG_SPMM_MINB_G2
+#define RG_SPMM_MINB_G2 5
+#endif
+template <int PB, int G>
 struct SpmmMinBlocks {
-  static constexpr int value = PB >= 16 ? 2 : 3;
+  static constexpr int value = G > 1 ? RG_SPMM_MINB_G2 : (PB >= 6 ? 2 : 3);
 };
 
-template <int PB, bool GHOST>
-__global__ void __launch_bounds__(kSpmmWarps * 32, SpmmMinBlocks<PB>::value)
+// G lanes share a row (each owns PB of the G*PB columns); units are 32/G rows.
+template <int PB, bool GHOST, int G = 1, int CH = kSpmmChunk>
+__global__ void __launch_bounds__(kSpmmWarps * 32, SpmmMinBlocks<PB, G>::value)
 spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
                     const int32_t* __restrict__ ci, const double* __restrict__ va,
                     const double* __restrict__ X, int64_t ldx, int64_t n_local,
                     const double* __restrict__ Xg, int64_t ldg, double* __restrict__ Y, int64_t ldy) {
-  __shared__ int32_t s_ci[kSpmmWarps][2][kSpmmChunk];
-  __shared__ double s_va[kSpmmWarps][2][kSpmmChunk];
+  constexpr int RPW = 32 / G;
+  __shared__ int32_t s_ci[kSpmmWarps][2][CH];
+  __shared__ double s_va[kSpmmWarps][2][CH];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int64_t nunits = (row_end - row_begin + 31) / 32;
+  const int cg = lane / RPW;
+  X += (int64_t)cg * PB * ldx;
+  if (GHOST) Xg += (int64_t)cg * PB * ldg;
+  Y += (int64_t)cg * PB * ldy;
+  const int64_t nunits = (row_end - row_begin + RPW - 1) / RPW;
   const int64_t nwarps = (int64_t)gridDim.x * kSpmmWarps;
   int64_t u = (int64_t)blockIdx.x * kSpmmWarps + w;
   if (u >= nunits) return;
 
   auto issue_csr = [&](const UnitRp& r, int buf) {
     const int32_t cnt = r.wend - r.wbeg;
-    if (cnt <= kSpmmChunk) {
+    if (cnt <= CH) {
       for (int e = lane; e < cnt; e += 32) {
         cp_async4(&s_ci[w][buf][e], ci + r.wbeg + e);
         cp_async8(&s_va[w][buf][e], va + r.wbeg + e);
@@ -221,10 +234,10 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 
-  UnitRp cur = load_unit_rp(rp, row_begin + u * 32, row_end, lane);
+  UnitRp cur = load_unit_rp<RPW>(rp, row_begin + u * RPW, row_end, lane);
   issue_csr(cur, 0);
   UnitRp nxt = cur;
-  if (u + nwarps < nunits) nxt = load_unit_rp(rp, row_begin + (u + nwarps) * 32, row_end, lane);
+  if (u + nwarps < nunits) nxt = load_unit_rp<RPW>(rp, row_begin + (u + nwarps) * RPW, row_end, lane);
   int buf = 0;
   for (; u < nunits; u += nwarps) {
     const bool has_next = u + nwarps < nunits;
@@ -233,23 +246,23 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
     __syncwarp();
     if (has_next) issue_csr(nxt, buf ^ 1);
     UnitRp nn = nxt;
-    if (u + 2 * nwarps < nunits) nn = load_unit_rp(rp, row_begin + (u + 2 * nwarps) * 32, row_end, lane);
+    if (u + 2 * nwarps < nunits) nn = load_unit_rp<RPW>(rp, row_begin + (u + 2 * nwarps) * RPW, row_end, lane);
 
-    const int64_t wrow0 = row_begin + u * 32;
-    const int64_t i = wrow0 + lane;
+    const int64_t wrow0 = row_begin + u * RPW;
+    const int64_t i = wrow0 + lane % RPW;
     double acc[PB];
 #pragma unroll
     for (int c = 0; c < PB; ++c) acc[c] = 0.0;
     const int32_t cnt = cur.wend - cur.wbeg;
-    if (cnt <= kSpmmChunk) {
+    if (cnt <= CH) {
       accumulate_rows<PB, GHOST>(s_ci[w][buf], s_va[w][buf], cur.mybeg - cur.wbeg, cur.myend - cur.wbeg, X, ldx,
                                  n_local, Xg, ldg, acc);
     } else {
       // long rows: chunked synchronous staging through this unit's buffer
       int32_t* sci = s_ci[w][buf];
       double* sva = s_va[w][buf];
-      for (int32_t base = cur.wbeg; base < cur.wend; base += kSpmmChunk) {
-        const int32_t c2 = min(kSpmmChunk, cur.wend - base);
+      for (int32_t base = cur.wbeg; base < cur.wend; base += CH) {
+        const int32_t c2 = min(CH, cur.wend - base);
         __syncwarp();
         for (int e = lane; e < c2; e += 32) {
           sci[e] = __ldg(ci + base + e);
@@ -271,6 +284,28 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
     buf ^= 1;
   }
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// G = 2 lanes per row, 16-row units with up to 128 staged entries each: twice
+// the warps in flight of the lane-per-row kernel at half the registers
+template <int PB>
+static void launch_spmm_g2(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double* va,
+                           const double* X, int64_t ldx, int64_t n_local, const double* Xg, int64_t ldg, double* Y,
+                           int64_t ldy, cudaStream_t s) {
+  static int per_sm[2] = {-1, -1};
+  const int gi = Xg ? 1 : 0;
+  auto k = Xg ? spmm_persist_kernel<PB, true, 2, 128> : spmm_persist_kernel<PB, false, 2, 128>;
+  if (per_sm[gi] < 0) {
+    int v = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kSpmmWarps * 32, 0);
+    per_sm[gi] = v < 1 ? 1 : v;
+  }
+  const int64_t units = (re - rb + 15) / 16;
+  int64_t g = (int64_t)sm_count() * per_sm[gi];
+  const int64_t need = (units + kSpmmWarps - 1) / kSpmmWarps;
+  if (need < g) g = need;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg, Y, ldy);
 }
 
 template <int PB>
@@ -333,6 +368,7 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
   // exact-width passes (no per-column predication in the inner loop) of at
   // most 8 columns: a 16-wide register block spills, and re-reading A for a
   // second 8-wide pass is cheaper (profiles/spmm_r01.txt)
+  static const int g2 = getenv("RG_SPMM_G2") ? atoi(getenv("RG_SPMM_G2")) : 0;
   for (int c0 = 0; c0 < p;) {
     const int rem = p - c0;
     const int pc = rem >= 8 ? 8 : rem;
@@ -347,7 +383,12 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
       case 5: launch_spmm<5>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 6: launch_spmm<6>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 7: launch_spmm<7>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
-      case 8: launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      case 8:
+        if (g2)
+          launch_spmm_g2<4>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
+        else
+          launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
+        break;
       default: launch_spmm<16>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
     }
     RG_CHECK_LAUNCH("rg_spmm_csr_f64");
