@@ -194,12 +194,9 @@ __device__ __forceinline__ void accumulate_rows(const int32_t* sci, const double
 // CTAs per SM the register budget is sized for: 3 (85 registers) spills at
 // PB >= 6, and the spill traffic costs more than the extra warps buy
 // (cfg4 p = 8: 912 us with 3, 824 us with 2; profiles/spmm_r01.txt)
-#ifndef RG_SPMM_MINB_G2
-#define RG_SPMM_MINB_G2 5
-#endif
 template <int PB, int G>
 struct SpmmMinBlocks {
-  static constexpr int value = G > 1 ? RG_SPMM_MINB_G2 : (PB >= 6 ? 2 : 3);
+  static constexpr int value = PB >= 6 ? 2 : (G > 1 ? 4 : 3);
 };
 
 // G lanes share a row (each owns PB of the G*PB columns); units are 32/G rows.
@@ -369,13 +366,19 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
   // most 8 columns: a 16-wide register block spills, and re-reading A for a
   // second 8-wide pass is cheaper (profiles/spmm_r01.txt)
   static const int g2 = getenv("RG_SPMM_G2") ? atoi(getenv("RG_SPMM_G2")) : 0;
+  static const int g2_16 = getenv("RG_SPMM_G2_16") ? atoi(getenv("RG_SPMM_G2_16")) : 0;
   for (int c0 = 0; c0 < p;) {
     const int rem = p - c0;
-    const int pc = rem >= 8 ? 8 : rem;
+    // RG_SPMM_G2_16=1: 16-wide passes with two lanes per row (A read once) -- 1.5x slower
+    // than two 8-wide passes at cfg4 (profiles/spmm_r01.txt), so off by default
+    const int pc = (rem >= 16 && g2_16) ? 16 : (rem >= 8 ? 8 : rem);
     const double* X = d_x ? d_x + (int64_t)c0 * ldx : nullptr;
     const double* Xg = d_xg ? d_xg + (int64_t)c0 * ldg : nullptr;
     double* Y = d_y + (int64_t)c0 * ldy;
     switch (pc) {
+      case 16:
+        launch_spmm_g2<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
+        break;
       case 1: launch_spmm<1>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 2: launch_spmm<2>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 3: launch_spmm<3>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
