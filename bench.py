@@ -58,6 +58,20 @@ def step_model_bytes(n, nnz, p=P_BLOCK, k=K_RECYCLE, j=M_STEPS - 1, esz=8):
     return spmm + cgs2 + qr, dict(spmm=spmm, cgs2=cgs2, qr=qr)
 
 
+def _ncu_traffic(label, family):
+    """DRAM bytes (read + write) per launch of the kernel with this launch
+    label, from the committed ncu --set full capture of the same step
+    (profiles/ncu_traffic_r01*.json, written by tools/ncu_traffic.py)."""
+    name = "ncu_traffic_r01.json" if family == "cfg4" else f"ncu_traffic_r01_{family}.json"
+    f = ROOT / "profiles" / name
+    if not f.exists():
+        return None, None
+    for rec in json.loads(f.read_text())["launches"]:
+        if rec["label"] == label:
+            return rec["traffic_bytes"], f"profiles/{name}"
+    return None, None
+
+
 def _peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -285,8 +299,10 @@ def run_ours(args, rank, world):
     top = kernels[0]
     top_gbs = top[3] / (top[2] * 1e-3) / 1e9
     total_ms = sum(k[2] for k in kernels)
+    traffic, traffic_src = _ncu_traffic(top[0], args.family)
     roofline = {"bound": "hbm", "achieved": top_gbs, "peak": peak, "unit": "GB/s", "frac": top_gbs / peak,
-                "traffic": None, "kernel": top[0], "kernel_share": top[2] / max(total_ms, 1e-9),
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": top[0],
+                "kernel_share": top[2] / max(total_ms, 1e-9),
                 "bytes_per_launch": top[3] // max(top[1], 1), "peak_source": peak_kind}
 
     # end to end through the reference-facing call with host buffers

@@ -5,6 +5,7 @@ so that ncu can capture the kernels of one step.
 """
 
 import argparse
+import json
 import pathlib
 import sys
 
@@ -19,17 +20,26 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=None)
     ap.add_argument("--family", default="cfg4")
+    ap.add_argument("--labels", default=None, help="write the launch labels of the profiled steps here")
     ap.add_argument("--steps", type=int, default=2)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     grid = args.grid or bench.FAMILIES[args.family]["grid"]
     _, op, rs, fact, _ = bench._setup_step(grid, dev, family=args.family)
     torch.cuda.synchronize()
+    from paper_1604_01713_b200 import device as D
+
+    D.LaunchLog.reset(timing=True)
     torch.cuda.cudart().cudaProfilerStart()
     for _ in range(args.steps):
         bench._one_step(fact, op, rs)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
+    # launch order of the profiled steps (tools/ncu_traffic.py pairs it with ncu's launch list)
+    recs = [{"label": lbl, "bytes": b} for lbl, b, _, _ in D.LaunchLog.records]
+    D.LaunchLog.reset(timing=False)
+    if args.labels:
+        pathlib.Path(args.labels).write_text(json.dumps(recs, indent=1))
     print("prof_step done")
 
 
