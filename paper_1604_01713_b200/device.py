@@ -372,6 +372,16 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
     if p > maxp:
         _tall_wide(Z_in, Z_out, terms, r1, r2, gram, n, p, cplx)
         return
+    if gram is not None and gram[0] == "self" and p > maxgc:
+        # a self Gram wider than one launch's Gram tiles: form z, then
+        # G[g0:g1, :] = z[:, g0:g1]^T z in basis-Gram chunks
+        dev = (Z_in if Z_in is not None else Z_out).device
+        zb = Z_out if Z_out is not None else empty_block(n, p, dev, torch.complex128 if cplx else torch.float64)
+        tall(Z_in, zb, terms, r1=r1, r2=r2, n=n, p=p)
+        for g0 in range(0, p, maxgc):
+            g1 = min(p, g0 + maxgc)
+            tall(zb, None, gram=("basis", zb[:, g0:g1], gram[1][g0:g1, :]), n=n, p=p)
+        return
     gmode, gb, gout = 0, None, None
     if gram is not None:
         kind = gram[0]

@@ -100,7 +100,7 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("n", [1, 255, 256, 1000, 100003])
-@pytest.mark.parametrize("p", [1, 3, 8, 16])
+@pytest.mark.parametrize("p", [1, 3, 8, 16, 20, 24, 32])
 def test_tall_gram_and_update(cuda, n, p):
     D = _dev()
     rng = np.random.default_rng(n + p)
@@ -126,6 +126,16 @@ def test_tall_gram_and_update(cuda, n, p):
     ss = torch.zeros(p, dtype=torch.float64, device=cuda)
     D.tall(Zo, None, gram=("sumsq", ss))
     assert _rel(ss.cpu().numpy(), (ref * ref).sum(axis=0)) <= 1e-12
+    # the fused CGS pass shape: update by one basis, Gram against another (split when wide)
+    X3 = rng.standard_normal((n, 140))
+    S3 = rng.standard_normal((140, p))
+    out = D.small(90, p)
+    Gb = rng.standard_normal((n, 90))
+    D.tall(Zd, Zo, [(D.to_device_block(X3), torch.from_numpy(S3).to(cuda), -1.0)],
+           gram=("basis", D.to_device_block(Gb), out))
+    ref = Z - X3 @ S3
+    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
+    assert _rel(out.cpu().numpy(), Gb.T @ ref) <= 1e-12
 
 
 @pytest.mark.parametrize("p", [1, 4, 8, 16, 20, 32])
