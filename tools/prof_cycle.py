@@ -71,5 +71,42 @@ def main():
     print(json.dumps(out, indent=1))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--recycle" not in sys.argv:
     main()
+
+
+def recycle_breakdown(grid=256):
+    """Per-launch device time of one end-of-cycle recycle update (after a
+    full cycle of system 0), plus its host time."""
+    from paper_1604_01713_b200 import SolverConfig, arnoldi, device as D, problems, solver
+
+    A, B, system, kw = problems.cfg4_sequence(N=grid, n_systems=1)
+    cfg = SolverConfig(**dict(kw, max_cycles=2))
+    captured = {}
+    orig = solver._update_space
+
+    def grab(fact, rs, cfg_, report):
+        captured["args"] = (fact, rs, cfg_, report)  # keep the last (augmented) call
+        return orig(fact, rs, cfg_, report)
+
+    solver._update_space = grab
+    solver.solve_block_gcrodr(system(0), B, None, cfg)
+    solver._update_space = orig
+    fact, rs, cfg_, report = captured["args"]
+    orig(fact, rs, cfg_, report)  # warm
+    torch.cuda.synchronize()
+    D.LaunchLog.reset(timing=True)
+    t0 = time.perf_counter()
+    orig(fact, rs, cfg_, report)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    summ = D.LaunchLog.summary()
+    D.LaunchLog.reset(timing=False)
+    dev_ms = sum(v[1] for v in summ.values())
+    print(json.dumps({"augmented_update_wall_ms": wall * 1e3, "device_ms": dev_ms,
+                      "launches": {k: [v[0], round(v[1], 3), round(v[2] / max(v[1], 1e-9) / 1e6, 1)]
+                                   for k, v in sorted(summ.items(), key=lambda kv: -kv[1][1])}}, indent=1))
+
+
+if __name__ == "__main__" and "--recycle" in sys.argv:
+    recycle_breakdown()
