@@ -55,7 +55,11 @@ class ArnoldiFactorization:
         self.m = 0
         dev = _dev.require_cuda(device)
         self.device = dev
-        self._W = _dev.empty_block(n, (m_max + 1) * L, dev, dtype)
+        # [C | W] in one allocation: C (copied in by start) directly precedes the
+        # basis, so the CGS2 projection can treat [C W] as one basis
+        self._CW = _dev.empty_block(n, k + (m_max + 1) * L, dev, dtype)
+        self._W = self._CW[:, k:]
+        self._c_src = None  # data_ptr of the recycle space C copied into _CW[:, :k]
         self._H = np.zeros(((m_max + 1) * L, m_max * L), dtype=npdt)
         self._F = np.zeros((k, m_max * L), dtype=npdt)
         self.z_bar = np.zeros((L, L), dtype=npdt)
@@ -196,6 +200,9 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     if recycle is not None and recycle.c_device().dtype != R0d.dtype:
         R0d = R0d.to(recycle.c_device().dtype) if R0d.dtype == torch.float64 else R0d
     fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev, R0d.dtype)
+    if recycle is not None and k:
+        fact._CW[:, :k].copy_(recycle.c_device())
+        fact._c_src = recycle.c_device().data_ptr()
     V1 = fact.v_block(0)
     qr = _block_qr(fact, R0d, V1)
     fact.z_bar = qr[0]
@@ -252,9 +259,40 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     scr = fact._qr
     Vnew = fact.v_block(m + 1)
 
-    if ortho == "cgs2":
+    k_, w_ = fact.k, (m + 1) * L
+    # [C W] as one basis when C sits in front of W (real data; the complex
+    # tall pass has no aliased-term merge): 3 passes instead of 5
+    joint = (ortho == "cgs2" and C is not None and k_ > 0 and fact._c_src == C.data_ptr()
+             and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
+    if ortho == "cgs2" and joint:
+        CW = fact._CW[:, : k_ + w_]
+        if _dev.fused_ok() and L <= _dev.MAX_P_FUSED:
+            # rg_cgs2_f64 sees C and W adjacent and runs the same three passes
+            _dev.cgs2(Ahat, fact._CW[:, :k_], active, fact._coef, scr.G1)
+        else:
+            kw = k_ + w_
+            G1 = fact._coef[: kw * L].view(L, kw).t()
+            G2 = fact._coef[kw * L: 2 * kw * L].view(L, kw).t()
+            _dev.tall(Ahat, None, gram=("basis", CW, G1))
+            _dev.tall(Ahat, None, [(CW, G1, -1.0)], gram=("basis", CW, G2))
+            _dev.tall(Ahat, Ahat, [(CW, G1, -1.0), (CW, G2, -1.0)],
+                      gram=("self", scr.G1) if L <= _dev.max_p(Ahat) else None)
+        ncoef = 2 * (k_ + w_) * L
+        fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
+        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.max_p(Ahat))
+        hc = fact._coef_host.numpy()
+        kw = k_ + w_
+        hG1 = hc[: kw * L].reshape(L, kw).T
+        hG2 = hc[kw * L: 2 * kw * L].reshape(L, kw).T
+        fact._F[:, cols] += hG1[:k_]
+        fact._F[:, cols] += hG2[:k_]
+        fact._H[: (m + 1) * L, cols] += hG1[k_:]
+        fact._H[: (m + 1) * L, cols] += hG2[k_:]
+    elif ortho == "cgs2":
         if _dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED and fact.k + (m + 1) * L <= 256:
-            # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64)
+            # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64);
+            # C is passed from its own allocation here, so the five-pass
+            # sequential schedule applies
             _dev.cgs2(Ahat, C, active, fact._coef, scr.G1)
         else:
             S1, c1, S2, c2 = fact._coef_views(m)

@@ -48,6 +48,24 @@ extern "C" int rg_cgs2_f64(int64_t n, int32_t p, double* d_z, int64_t ldz, const
   RG_REQUIRE(k >= 0 && w >= 0 && (k == 0 || d_c) && (w == 0 || d_w) && d_z && d_coef,
              "rg_cgs2_f64: bad operands");
   RG_REQUIRE(k + w <= 256, "rg_cgs2_f64: k + w = %d too wide for one schedule", k + w);
+  if (k > 0 && w > 0 && d_w == d_c + (int64_t)k * ldc && ldw == ldc && k + w <= 128) {
+    // C and W adjacent in one allocation: project against [C W] as one basis
+    // (C is orthogonal to W, so this is the same CGS2 up to rounding):
+    //   P1  G1 = [C W]^T z
+    //   P2  G2 = [C W]^T (z - [C W] G1)
+    //   P3  z <- z - [C W] (G1 + G2)  (aliased terms merged), self Gram
+    // three passes instead of five.  Coefficients: G1 | G2, each (k+w) x p.
+    const int kw = k + w;
+    double* G1 = d_coef;
+    double* G2 = d_coef + (int64_t)kw * p;
+    int rc = tall_call(n, p, d_z, ldz, nullptr, ldz, {}, 1, d_c, ldc, kw, G1, d_work, work_bytes, stream);
+    if (rc) return rc;
+    rc = tall_call(n, p, d_z, ldz, nullptr, ldz, {{d_c, ldc, kw, G1}}, 1, d_c, ldc, kw, G2, d_work, work_bytes,
+                   stream);
+    if (rc) return rc;
+    return tall_call(n, p, d_z, ldz, d_z, ldz, {{d_c, ldc, kw, G1}, {d_c, ldc, kw, G2}}, d_gram ? 2 : 0, nullptr, 1,
+                     p, d_gram, d_work, work_bytes, stream);
+  }
   // coefficient blocks S1 | c1 | S2 | c2 packed column-major in d_coef
   std::vector<Basis> bases;
   double* off = d_coef;

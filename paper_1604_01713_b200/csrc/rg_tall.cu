@@ -68,6 +68,7 @@ struct TallParams {
   double* part;            // [grid][gc*p] (modes 1/2) or [grid][p] (mode 3)
   unsigned int* counter;   // ticket
   int64_t ntiles;
+  int merge12;             // v6: terms 1 and 2 share X -> one term with alpha1 S1 + alpha2 S2
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -803,6 +804,7 @@ static int pick_mtmax(int mtiles) {
   if (mtiles <= 2) return 2;
   if (mtiles <= 6) return 6;
   if (mtiles <= 12) return 12;
+  if (mtiles <= 13) return 13;  // [C W] = 20 + 80 columns (cfg4 joint projection)
   return 16;
 }
 
@@ -887,7 +889,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   extern __shared__ __align__(16) double smem[];
   __shared__ SlabTab tab;
   const int p = P.p;
-  const int ks1 = (P.a1 + 3) / 4, ks2 = (P.a2 + 3) / 4;
+  const int ks1 = (P.a1 + 3) / 4, ks2 = P.merge12 ? 0 : (P.a2 + 3) / 4;
   double* sf1 = smem;                          // [ks1][NT][32] DMMA B fragments of S1
   double* sf2 = sf1 + (size_t)ks1 * NT * 32;   // [ks2][NT][32]
   double* sR1 = sf2 + (size_t)ks2 * NT * 32;   // PM x PM row-major, reciprocal diagonal
@@ -899,7 +901,13 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   for (int e = threadIdx.x; e < ks1 * NT * 32; e += kV6Threads) {
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
     const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
-    sf1[e] = (aa < P.a1 && c < p) ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
+    double v = 0.0;
+    if (aa < P.a1 && c < p) {
+      v = P.s1[aa + (int64_t)c * P.a1];
+      // aliased terms: one pass over X with the combined coefficients
+      if (P.merge12) v = P.alpha1 * v + P.alpha2 * P.s2[aa + (int64_t)c * P.a2];
+    }
+    sf1[e] = v;
   }
   for (int e = threadIdx.x; e < ks2 * NT * 32; e += kV6Threads) {
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
@@ -1077,7 +1085,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
         }
         release();
       }
-      const double alpha = t == 0 ? P.alpha1 : P.alpha2;
+      const double alpha = t == 0 ? (P.merge12 ? 1.0 : P.alpha1) : P.alpha2;
 #pragma unroll
       for (int rg = 0; rg < 4; ++rg)
 #pragma unroll
@@ -1131,6 +1139,12 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
         }
       }
     } else {
+      // the z-tile B fragments are the same for every Gram row tile: load once
+      double bz[8][NT];
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bz[ks][nt] = zt[(nt * 8 + mrow) * kSS6 + ks * 4 + kq];
 #pragma unroll
       for (int mt = 0; mt < MTA; ++mt) {
         if (mt < mtiles) {
@@ -1139,8 +1153,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
           for (int ks = 0; ks < 8; ++ks) {
             const double a = sl[mrow * kSS6 + ks * 4 + kq];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-              dmma(acc[mt][nt][0], acc[mt][nt][1], a, zt[(nt * 8 + mrow) * kSS6 + ks * 4 + kq]);
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a, bz[ks][nt]);
           }
           release();
         }
@@ -1218,10 +1231,10 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
   SlabPlan L;
   L.nz = P.zin ? (P.p + 7) / 8 : 0;
   L.n1 = (P.a1 + 7) / 8;
-  L.n2 = (P.a2 + 7) / 8;
+  L.n2 = P.merge12 ? 0 : (P.a2 + 7) / 8;
   L.ng = P.gmode == 1 ? (P.gc + 7) / 8 : 0;
   L.total = L.nz + L.n1 + L.n2 + L.ng;
-  const int ks1 = (P.a1 + 3) / 4, ks2 = (P.a2 + 3) / 4;
+  const int ks1 = (P.a1 + 3) / 4, ks2 = P.merge12 ? 0 : (P.a2 + 3) / 4;
   const size_t smem = ((size_t)(ks1 + ks2) * NT * 32 + 2 * PM * PM + 2 + (size_t)kV6Warps * kWarpWords +
                        (size_t)std::max(MTMAX * NT * 64, kV6Warps * PM)) * sizeof(double);
   static int per_sm = -1;
@@ -1248,6 +1261,7 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
       case 2: e = launch_v6<PMv, 2>(P, bound, st); break;                                 \
       case 6: e = launch_v6<PMv, 6>(P, bound, st); break;                                 \
       case 12: e = launch_v6<PMv, 12>(P, bound, st); break;                               \
+      case 13: e = launch_v6<PMv, 13>(P, bound, st); break;                               \
       default: e = launch_v6<PMv, 16>(P, bound, st); break;                               \
     }                                                                                     \
     break;
@@ -1392,6 +1406,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   P.counter = (unsigned int*)d_work;
   P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
   P.ntiles = (n + kTallThreads - 1) / kTallThreads;
+  P.merge12 = 0;
   if (gram_mode == 0 && P.ntiles == 0) return RG_OK;
   const int PM = pick_pm(p);
   const int mtmax = pick_mtmax(P.mtiles);
@@ -1410,6 +1425,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
                "rg_tall_f64: p=%d > 16 needs 16-byte aligned operands, <= 128 term columns, <= %d slabs", p,
                kMaxSlabs);
     const int mtw = P.mtiles == 0 ? 0 : (P.mtiles <= 2 ? 2 : 4);
+    P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
     if (PM == 24)
       e = mtw == 0 ? launch_v6<24, 0>(P, bound, st) : (mtw == 2 ? launch_v6<24, 2>(P, bound, st)
                                                                   : launch_v6<24, 4>(P, bound, st));
@@ -1433,7 +1449,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
     int which = 6;
     if (a1 + a2 == 0) {
       if (gram_mode == 1)
-        which = 5;
+        which = P.mtiles > 12 ? 6 : 5;  // v5 spills with more than 96 Gram rows; v6<PM, 13> does not
       else if (gram_mode == 2 && (d_r1 || d_r2))
         which = 3;
     }
@@ -1441,6 +1457,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
     const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     if (which == 6 && ncol_slabs <= kMaxSlabs) {
+      P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
       switch (PM) {
         RG_V6_CASE(1)
         RG_V6_CASE(2)

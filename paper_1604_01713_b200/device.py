@@ -305,7 +305,9 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
         # a Gram basis that aliases an update operand is streamed once
         aliased = gmode == 1 and any(x is not None and x.data_ptr() == gb.data_ptr() and gc <= x.shape[1]
                                      for x in (x1, x2))
-        cols = ((p if zin is not None else 0) + a1 + a2 + (gc if gmode == 1 and not aliased else 0)
+        # two terms over the same operand are merged into one pass over it (rg_tall v6)
+        same_x = x1 is not None and x2 is not None and x1.data_ptr() == x2.data_ptr() and a1 == a2
+        cols = ((p if zin is not None else 0) + a1 + (0 if same_x else a2) + (gc if gmode == 1 and not aliased else 0)
                 + (p if zout is not None and (zin is None or zout.data_ptr() != zin.data_ptr()) else p if zout is not None else 0))
         label = (f"rg_tall p={p} in={int(zin is not None)} a={a1}+{a2} "
                  f"g{gmode}:{gc} trsm={int(r1 is not None) + int(r2 is not None)} out={int(zout is not None)}")
@@ -497,11 +499,13 @@ def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1) -> None:
     n, p = Z.shape
     k = 0 if C is None else C.shape[1]
     w = W.shape[1]
-    ws = Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k, w, p)))
+    ws = Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k + w, p)))
     rc = L.rg_cgs2_f64(n, p, Z.data_ptr(), ld_of(Z), ptr(C), ld_of(C) if C is not None else 1, k,
                        W.data_ptr(), ld_of(W), w, coef.data_ptr(), ptr(G1), ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check(rc, "cgs2")
-    LaunchLog.count += (2 if k else 0) + (2 if w else 0) + 1
+    joint = (k and w and ld_of(C) == ld_of(W) and W.data_ptr() == C.data_ptr() + k * ld_of(C) * C.element_size()
+             and k + w <= MAX_GC)
+    LaunchLog.count += 3 if joint else (2 if k else 0) + (2 if w else 0) + 1
 
 
 def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch.Tensor, gram_ready: bool) -> None:
