@@ -880,12 +880,12 @@ struct SlabTab {
   int nv[kMaxSlabs][2];             // valid 16-byte chunks per column parity (0..4)
 };
 
-template <int PM, int MTMAX>
-__global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(TallParams P, SlabPlan L) {
+template <int PM, int MTMAX, int W6 = kV6Warps, int R6 = kRing6>
+__global__ void __launch_bounds__(W6 * 32, PM > 16 ? 1 : 2) tall_v6_kernel(TallParams P, SlabPlan L) {
   constexpr int PM8 = PM < 8 ? 8 : PM;
   constexpr int NT = PM8 / 8;
   constexpr int MTA = MTMAX > 0 ? MTMAX : 1;
-  constexpr int kWarpWords = kRing6 * 8 * kSS6 + PM8 * kSS6;
+  constexpr int kWarpWords = R6 * 8 * kSS6 + PM8 * kSS6;
   extern __shared__ __align__(16) double smem[];
   __shared__ SlabTab tab;
   const int p = P.p;
@@ -896,9 +896,9 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   double* sR2 = sR1 + PM * PM;
   double* wbase = sR2 + PM * PM;
   wbase += ((uintptr_t)wbase & 15) ? 1 : 0;
-  double* red = wbase + kV6Warps * kWarpWords;
+  double* red = wbase + W6 * kWarpWords;
 
-  for (int e = threadIdx.x; e < ks1 * NT * 32; e += kV6Threads) {
+  for (int e = threadIdx.x; e < ks1 * NT * 32; e += (W6 * 32)) {
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
     const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
     double v = 0.0;
@@ -909,18 +909,18 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
     }
     sf1[e] = v;
   }
-  for (int e = threadIdx.x; e < ks2 * NT * 32; e += kV6Threads) {
+  for (int e = threadIdx.x; e < ks2 * NT * 32; e += (W6 * 32)) {
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
     const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
     sf2[e] = (aa < P.a2 && c < p) ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
   }
-  for (int e = threadIdx.x; e < PM * PM; e += kV6Threads) {
+  for (int e = threadIdx.x; e < PM * PM; e += (W6 * 32)) {
     const int ii = e / PM, jj = e % PM;
     const double id = ii == jj ? 1.0 : 0.0;
     sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
     sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
   }
-  for (int k = threadIdx.x; k < L.total; k += kV6Threads) {
+  for (int k = threadIdx.x; k < L.total; k += (W6 * 32)) {
     const double* ptr;
     int64_t ld;
     int nc;
@@ -946,8 +946,8 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mrow = lane >> 2, kq = lane & 3;
-  double* ring = wbase + warp * kWarpWords;   // [kRing6][8][kSS6]
-  double* zt = ring + kRing6 * 8 * kSS6;      // [PM8][kSS6]  (column-major tile: zt[c*kSS6 + row])
+  double* ring = wbase + warp * kWarpWords;   // [R6][8][kSS6]
+  double* zt = ring + R6 * 8 * kSS6;      // [PM8][kSS6]  (column-major tile: zt[c*kSS6 + row])
   const bool gram_tile = MTMAX > 0 && (P.gmode == 1 || P.gmode == 2);
   const int mtiles = P.mtiles;
 
@@ -961,8 +961,8 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   for (int c = 0; c < PM; ++c) sq[c] = 0.0;
 
   const int64_t nunits = (P.n + 31) / 32;
-  const int64_t gwarp = (int64_t)blockIdx.x * kV6Warps + warp;
-  const int64_t nwarps = (int64_t)gridDim.x * kV6Warps;
+  const int64_t gwarp = (int64_t)blockIdx.x * W6 + warp;
+  const int64_t nwarps = (int64_t)gridDim.x * W6;
   const int64_t my_units = gwarp < nunits ? (nunits - gwarp + nwarps - 1) / nwarps : 0;
 
   // per-lane chunk geometry: chunk t covers column (lane>>4) + 2t, rows 2*(lane&15) .. +1
@@ -975,7 +975,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   const uint32_t dst_lane =
       static_cast<uint32_t>(__cvta_generic_to_shared(ring + ccol * kSS6 + rp2));
   uint32_t dst_slot = dst_lane;
-  const uint32_t dst_wrap = dst_lane + kRing6 * 8 * kSS6 * 8;
+  const uint32_t dst_wrap = dst_lane + R6 * 8 * kSS6 * 8;
   auto row_bytes = [&](int64_t row) {
     const int64_t vr = P.n - row;
     return vr >= 2 ? 16 : (vr == 1 ? 8 : 0);
@@ -1020,13 +1020,13 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
     if (dst_slot == dst_wrap) dst_slot = dst_lane;
   };
 #pragma unroll
-  for (int s = 0; s < kRing6; ++s) issue_next();
+  for (int s = 0; s < R6; ++s) issue_next();
   int cons_slot = 0;
   auto acquire = [&]() -> const double* {
-    cp_async_wait<kRing6 - 1>();
+    cp_async_wait<R6 - 1>();
     __syncwarp();
     const double* s = ring + cons_slot * 8 * kSS6;
-    if (++cons_slot == kRing6) cons_slot = 0;
+    if (++cons_slot == R6) cons_slot = 0;
     return s;
   };
   auto release = [&]() {
@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   __shared__ bool s_last;
   __syncthreads();
   if (gram_tile) {
-    for (int ww = 0; ww < kV6Warps; ++ww) {
+    for (int ww = 0; ww < W6; ++ww) {
       if (warp == ww) {
 #pragma unroll
         for (int mt = 0; mt < MTA; ++mt)
@@ -1184,7 +1184,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
       __syncthreads();
     }
     const int ne = P.gc * p;
-    for (int e = threadIdx.x; e < ne; e += kV6Threads) {
+    for (int e = threadIdx.x; e < ne; e += (W6 * 32)) {
       const int gg = e % P.gc, c = e / P.gc;
       const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
       const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
@@ -1197,9 +1197,9 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
 #pragma unroll
       for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
     __syncthreads();
-    for (int c = threadIdx.x; c < p; c += kV6Threads) {
+    for (int c = threadIdx.x; c < p; c += (W6 * 32)) {
       double sum = 0.0;
-      for (int ww = 0; ww < kV6Warps; ++ww) sum += red[ww * PM + c];
+      for (int ww = 0; ww < W6; ++ww) sum += red[ww * PM + c];
       P.part[(int64_t)blockIdx.x * p + c] = sum;
     }
   }
@@ -1214,7 +1214,7 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   if (!s_last) return;
   __threadfence();
   const int ne = (P.gmode == 3) ? p : P.gc * p;
-  for (int e = threadIdx.x; e < ne; e += kV6Threads) {
+  for (int e = threadIdx.x; e < ne; e += (W6 * 32)) {
     double sum = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
@@ -1222,12 +1222,12 @@ __global__ void __launch_bounds__(kV6Threads, PM > 16 ? 1 : 2) tall_v6_kernel(Ta
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
-template <int PM, int MTMAX>
+template <int PM, int MTMAX, int W6 = kV6Warps, int R6 = kRing6>
 static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t st) {
   constexpr int PM8 = PM < 8 ? 8 : PM;
   constexpr int NT = PM8 / 8;
-  constexpr int kWarpWords = kRing6 * 8 * kSS6 + PM8 * kSS6;
-  auto k = tall_v6_kernel<PM, MTMAX>;
+  constexpr int kWarpWords = R6 * 8 * kSS6 + PM8 * kSS6;
+  auto k = tall_v6_kernel<PM, MTMAX, W6, R6>;
   SlabPlan L;
   L.nz = P.zin ? (P.p + 7) / 8 : 0;
   L.n1 = (P.a1 + 7) / 8;
@@ -1235,34 +1235,44 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
   L.ng = P.gmode == 1 ? (P.gc + 7) / 8 : 0;
   L.total = L.nz + L.n1 + L.n2 + L.ng;
   const int ks1 = (P.a1 + 3) / 4, ks2 = P.merge12 ? 0 : (P.a2 + 3) / 4;
-  const size_t smem = ((size_t)(ks1 + ks2) * NT * 32 + 2 * PM * PM + 2 + (size_t)kV6Warps * kWarpWords +
-                       (size_t)std::max(MTMAX * NT * 64, kV6Warps * PM)) * sizeof(double);
+  const size_t smem = ((size_t)(ks1 + ks2) * NT * 32 + 2 * PM * PM + 2 + (size_t)W6 * kWarpWords +
+                       (size_t)std::max(MTMAX * NT * 64, W6 * PM)) * sizeof(double);
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kV6Threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, (W6 * 32), smem);
     per_sm = v < 1 ? 1 : v;
   }
   const int64_t nunits = (P.n + 31) / 32;
   int64_t g = (int64_t)sm_count() * per_sm;
   if (g > max_grid) g = max_grid;
-  const int64_t need = (nunits + kV6Warps - 1) / kV6Warps;
+  const int64_t need = (nunits + W6 - 1) / W6;
   if (need < g) g = need;
   if (g < 1) g = 1;
-  k<<<(unsigned)g, kV6Threads, smem, st>>>(P, L);
+  k<<<(unsigned)g, (W6 * 32), smem, st>>>(P, L);
   return cudaGetLastError();
 }
 
+// Passes without a basis Gram (update / store / self-Gram) run 4-warp CTAs
+// with an 8-deep slab ring; passes streaming a Gram basis keep 8 warps x 4
+// (profiles/v6_study_r01.txt: 2.97 -> 2.68 ms for the final CGS2 pass).
 #define RG_V6_CASE(PMv)                                                                   \
   case PMv:                                                                               \
-    switch (mt5) {                                                                        \
-      case 0: e = launch_v6<PMv, 0>(P, bound, st); break;                                 \
-      case 2: e = launch_v6<PMv, 2>(P, bound, st); break;                                 \
-      case 6: e = launch_v6<PMv, 6>(P, bound, st); break;                                 \
-      case 12: e = launch_v6<PMv, 12>(P, bound, st); break;                               \
-      case 13: e = launch_v6<PMv, 13>(P, bound, st); break;                               \
-      default: e = launch_v6<PMv, 16>(P, bound, st); break;                               \
+    if (wide_ring) {                                                                      \
+      switch (mt5) {                                                                      \
+        case 0: e = launch_v6<PMv, 0, 4, 8>(P, bound, st); break;                         \
+        default: e = launch_v6<PMv, 2, 4, 8>(P, bound, st); break;                        \
+      }                                                                                   \
+    } else {                                                                              \
+      switch (mt5) {                                                                      \
+        case 0: e = launch_v6<PMv, 0>(P, bound, st); break;                               \
+        case 2: e = launch_v6<PMv, 2>(P, bound, st); break;                               \
+        case 6: e = launch_v6<PMv, 6>(P, bound, st); break;                               \
+        case 12: e = launch_v6<PMv, 12>(P, bound, st); break;                             \
+        case 13: e = launch_v6<PMv, 13>(P, bound, st); break;                             \
+        default: e = launch_v6<PMv, 16>(P, bound, st); break;                             \
+      }                                                                                   \
     }                                                                                     \
     break;
 
@@ -1458,6 +1468,8 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     if (which == 6 && ncol_slabs <= kMaxSlabs) {
       P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
+      static const int wide_env = getenv("RG_V6_WIDE") ? atoi(getenv("RG_V6_WIDE")) : 1;
+      const bool wide_ring = wide_env && gram_mode != 1 && PM <= 8 && P.mtiles <= 2 && !d_r1 && !d_r2 && a1 > 0;
       switch (PM) {
         RG_V6_CASE(1)
         RG_V6_CASE(2)
