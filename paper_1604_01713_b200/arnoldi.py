@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import device as _dev
-from .dense_kernels import QrScratch, _flags, cholqr2_finish, cholqr2_launch, tsqr_into
+from .dense_kernels import (TSQR_MAX_P, QrScratch, _flags, cholqr2_finish, cholqr2_launch, reduced_qr_device,
+                            tsqr_into)
 from .ortho import project_chain
 from .sparse_core import ShapeError
 
@@ -235,6 +236,10 @@ def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_r
         if ok:
             return R, _flags(R, norm_x, fact.rank_tol)
     else:
+        if L > (_dev.MAX_P_C if X.dtype == torch.complex128 else TSQR_MAX_P):
+            # wider than one TSQR: column panels (dense_kernels._wide_qr)
+            f = reduced_qr_device(X, fact.rank_tol, Q=Q)
+            return f.r_factor, f.flagged
         ss = torch.empty(L, dtype=torch.float64, device=X.device)
         _dev.tall(X, None, gram=("sumsq", ss))
         norm_x = float(np.sqrt(ss.sum().item()))

@@ -247,3 +247,18 @@ def test_device_inputs_and_outputs(cuda):
     X1, r1, _ = solve_block_gcrodr(A, B, None, SolverConfig(m=8, k=4, tol=1e-10))
     X2, r2, _ = solve_block_gcrodr(A, torch.from_numpy(B).to(cuda), None, SolverConfig(m=8, k=4, tol=1e-10))
     assert np.array_equal(X1, X2) and r1.matvec_count == r2.matvec_count
+
+
+@pytest.mark.parametrize("p", [12, 20, 36])
+def test_wide_blocks_solve(cuda, p):
+    """Block widths beyond one tall launch (p > 16: wide tiles; p > 32:
+    column-blocked passes) through the whole GCRO-DR path."""
+    from paper_1604_01713_b200 import SolverConfig, solve_block_gcrodr
+
+    A = _mat(400, 0.02, 140 + p, 3.0)
+    B = _rhs(400, p, 141 + p)
+    X, rep, rs = solve_block_gcrodr(A, B, None, SolverConfig(m=4, k=6, tol=1e-9, max_cycles=40))
+    assert rep.converged
+    assert np.linalg.norm(B - _dense(A) @ X) <= 1e-8 * np.linalg.norm(B)
+    U, C = rs.numpy()
+    assert np.linalg.norm(C.T @ C - np.eye(rs.k)) <= 1e-10 * rs.k
