@@ -135,7 +135,9 @@ class CsrMatrix:
 
     @classmethod
     def from_coo(cls, n_rows, n_cols, rows, cols, vals) -> "CsrMatrix":
-        m = sp.coo_matrix((np.asarray(vals, dtype=np.float64), (rows, cols)), shape=(n_rows, n_cols)).tocsr()
+        v = np.asarray(vals)
+        v = v.astype(np.complex128 if np.iscomplexobj(v) else np.float64)  # complex kept (config 5 extension)
+        m = sp.coo_matrix((v, (rows, cols)), shape=(n_rows, n_cols)).tocsr()
         m.sort_indices()
         return cls.from_scipy(m)
 
@@ -143,8 +145,8 @@ class CsrMatrix:
     def from_scipy(cls, m) -> "CsrMatrix":
         m = sp.csr_matrix(m)
         m.sort_indices()
-        return cls(m.shape[0], m.shape[1], m.indptr.copy(), m.indices.copy(),
-                   np.asarray(m.data, dtype=np.float64).copy())
+        data = np.asarray(m.data, dtype=np.complex128 if np.iscomplexobj(m.data) else np.float64)
+        return cls(m.shape[0], m.shape[1], m.indptr.copy(), m.indices.copy(), data.copy())
 
     def astype_complex(self) -> "CsrMatrix":
         """The same pattern with complex128 values (real matrix, complex blocks)."""

@@ -262,3 +262,38 @@ def test_wide_blocks_solve(cuda, p):
     assert np.linalg.norm(B - _dense(A) @ X) <= 1e-8 * np.linalg.norm(B)
     U, C = rs.numpy()
     assert np.linalg.norm(C.T @ C - np.eye(rs.k)) <= 1e-10 * rs.k
+
+
+def test_complex_driver_paths(cuda):
+    """Complex GMRES, complex enlargement of a single right-hand side, MGS,
+    and a real matrix with a complex right-hand side."""
+    from paper_1604_01713_b200 import CsrMatrix, SolverConfig, solve_block_gcrodr, solve_block_gmres
+
+    g = np.random.default_rng(150)
+    n = 300
+    M = sp.random(n, n, density=0.02, random_state=g, format="csr") * (1 + 0.5j) + (4 + 1j) * sp.eye(n)
+    A = CsrMatrix.from_scipy(sp.csr_matrix(M))
+    Ad = M.toarray()
+    B = g.standard_normal((n, 2)) + 1j * g.standard_normal((n, 2))
+    X, rep, _ = solve_block_gmres(A, B, cfg=SolverConfig(m=10, tol=1e-10, max_cycles=30))
+    assert rep.converged and np.linalg.norm(B - Ad @ X) <= 1e-9 * np.linalg.norm(B)
+    b = B[:, :1]
+    X, rep, _ = solve_block_gcrodr(A, b, None, SolverConfig(m=6, k=4, block_width=3, tol=1e-10, max_cycles=40))
+    assert rep.converged and np.linalg.norm(b - Ad @ X) <= 1e-9 * np.linalg.norm(b)
+    X, rep, _ = solve_block_gcrodr(A, B, None, SolverConfig(m=6, k=4, tol=1e-10, ortho="mgs", max_cycles=40))
+    assert rep.converged and np.linalg.norm(B - Ad @ X) <= 1e-9 * np.linalg.norm(B)
+    Ar = _mat(n, 0.02, 151, 4.0)
+    X, rep, _ = solve_block_gcrodr(Ar, B, None, SolverConfig(m=6, k=4, tol=1e-10, max_cycles=40))
+    assert np.iscomplexobj(X) and rep.converged
+    assert np.linalg.norm(B - _dense(Ar) @ X) <= 1e-9 * np.linalg.norm(B)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 33])
+def test_tiny_systems(cuda, n):
+    from paper_1604_01713_b200 import SolverConfig, solve_block_gcrodr
+
+    A = _mat(n, 0.5, 160 + n, 3.0)
+    B = _rhs(n, 1, 161)
+    X, rep, _ = solve_block_gcrodr(A, B, None, SolverConfig(m=4, k=2, tol=1e-12, max_cycles=20))
+    assert rep.converged
+    assert np.linalg.norm(B - _dense(A) @ X) <= 1e-11 * np.linalg.norm(B)
