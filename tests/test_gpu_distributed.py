@@ -46,3 +46,35 @@ def _cfg1_worker(rank, world):
 
 def test_cfg1_sequence_two_ranks_one_gpu(cuda):
     _run(2, _cfg1_worker)
+
+
+def _cfg5_worker(rank, world):
+    """Complex (config-5 shaped) sequence, row-partitioned over two ranks,
+    against the same sequence solved by one process."""
+    import torch
+
+    from paper_1604_01713_b200 import SolverConfig, distributed, problems, solve_sequence
+
+    torch.cuda.set_device(0)
+    system, B, kw = problems.cfg5_sequence(N=10, p=4)
+    cfg = SolverConfig(**dict(kw, k=6))
+    mats = [system(i) for i in range(2)]
+    ref = solve_sequence([(A, B) for A in mats], cfg)  # same process, no partition
+    dist_systems = []
+    part = None
+    for A in mats:
+        op, part = distributed.setup(A, align=100)
+        dist_systems.append((op, B))
+    reps = solve_sequence(dist_systems, cfg)
+    bn = np.linalg.norm(B)
+    for r, rr in zip(reps, ref):
+        assert r.error is None, r.error
+        assert r.converged and r.cycles == rr.cycles and r.matvec_count == rr.matvec_count
+        h, hr = np.concatenate(r.residual_history), np.concatenate(rr.residual_history)
+        assert np.abs(h - hr).max() <= 1e-9 * bn
+        assert np.abs(r.solution - rr.solution[part.r0:part.r1]).max() <= 1e-8 * np.abs(rr.solution).max()
+    distributed.teardown()
+
+
+def test_complex_sequence_two_ranks_one_gpu(cuda):
+    _run(2, _cfg5_worker)
