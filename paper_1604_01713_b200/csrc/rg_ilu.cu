@@ -75,19 +75,41 @@ __device__ __forceinline__ int32_t claim_chunk(unsigned* ticket, int lane) {
   return (int32_t)__shfl_sync(0xffffffffu, t, 0);
 }
 
+// all of a row's dependency flags are polled together (one L2 round trip per
+// poll instead of one per dependency)
+__device__ __forceinline__ void wait_rows(const int* flags, const int32_t* __restrict__ ci, int32_t eb, int32_t ee,
+                                          int epoch, unsigned ns_max) {
+  unsigned ns = 16;
+  for (;;) {
+    bool ready = true;
+    for (int32_t e = eb; e < ee; e += 4) {
+      int f[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) f[q] = e + q < ee ? ld_relaxed(flags + ci[e + q]) : epoch;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ready = ready && f[q] == epoch;
+    }
+    if (ready) return;
+    if (ns_max) {
+      __nanosleep(ns);
+      if (ns < ns_max) ns <<= 1;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kWaveWarps * 32) ilu0_kernel(Wave W, const int32_t* __restrict__ rp,
                                                                 const int32_t* __restrict__ ci, double* vals,
                                                                 const int32_t* __restrict__ dpos,
                                                                 long long* zero_row) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    const int32_t c = claim_chunk(W.ticket, lane);
-    if (c >= W.nchunks) return;
+  int32_t c = claim_chunk(W.ticket, lane);
+  while (c < W.nchunks) {
+    const int32_t c_next = claim_chunk(W.ticket, lane);  // overlaps this chunk
     const int32_t e1 = W.chunk[c + 1];
     for (int32_t ee_ = W.chunk[c] + lane; ee_ < e1; ee_ += 32) {
     const int32_t i = W.order[ee_];
     const int32_t lo = rp[i], hi = rp[i + 1], di = dpos[i];
-    for (int32_t t = lo; t < di; ++t) wait_row(W.flags, ci[t], W.epoch, W.ns_max);
+    wait_rows(W.flags, ci, lo, di, W.epoch, W.ns_max);
     fence_acquire();
     for (int32_t t = lo; t < di; ++t) {
       const int32_t k = ci[t];
@@ -108,6 +130,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) ilu0_kernel(Wave W, const int
     if (vals[di] == 0.0) atomicMin(zero_row, (long long)i);
     st_release(W.flags + i, W.epoch);
     }
+    c = c_next;
   }
 }
 
@@ -119,16 +142,16 @@ __global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_kernel(Wave W, const i
                                                                   const double* B, int64_t ldb, double* X,
                                                                   int64_t ldx) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    const int32_t c = claim_chunk(W.ticket, lane);
-    if (c >= W.nchunks) return;
+  int32_t c = claim_chunk(W.ticket, lane);
+  while (c < W.nchunks) {
+    const int32_t c_next = claim_chunk(W.ticket, lane);
     const int32_t e1 = W.chunk[c + 1];
     for (int32_t ee_ = W.chunk[c] + lane; ee_ < e1; ee_ += 32) {
     const int32_t i = W.order[ee_];
     const int32_t di = dpos[i];
     const int32_t eb = UPPER ? di + 1 : rp[i];
     const int32_t ee = UPPER ? rp[i + 1] : di;
-    for (int32_t e = eb; e < ee; ++e) wait_row(W.flags, ci[e], W.epoch, W.ns_max);
+    wait_rows(W.flags, ci, eb, ee, W.epoch, W.ns_max);
     fence_acquire();
     const double dinv_src = UPPER ? vals[di] : 1.0;
     for (int c0 = 0; c0 < p; c0 += 8) {
@@ -148,6 +171,7 @@ __global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_kernel(Wave W, const i
     }
     st_release(W.flags + i, W.epoch);
     }
+    c = c_next;
   }
 }
 
@@ -164,39 +188,43 @@ __global__ void __launch_bounds__(kWaveWarps * 32) sptrsv_perm_kernel(Wave W, co
                                                                        const double* __restrict__ dval, int p,
                                                                        double* Xw) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    const int32_t c = claim_chunk(W.ticket, lane);
-    if (c >= W.nchunks) return;
+  int32_t c = claim_chunk(W.ticket, lane);
+  while (c < W.nchunks) {
+    // claim the next chunk now: the ticket round trip overlaps this chunk
+    const int32_t c_next = claim_chunk(W.ticket, lane);
     const int32_t ce = W.chunk[c + 1];
-    // all rows of this lane (same level) first wait, then one acquire fence
-    for (int32_t r = W.chunk[c] + lane; r < ce; r += 32)
-      for (int32_t e = rp[r]; e < rp[r + 1]; ++e) wait_row(W.flags, ci[e], W.epoch, W.ns_max);
-    fence_acquire();
     for (int32_t r = W.chunk[c] + lane; r < ce; r += 32) {
-    const int32_t eb = rp[r], ee = rp[r + 1];
-    double* xr = Xw + (int64_t)r * p;
-    for (int c0 = 0; c0 < p; c0 += 8) {
-      double acc[8];
+      const int32_t eb = rp[r], ee = rp[r + 1];
+      double* xr = Xw + (int64_t)r * p;
+      // the row's own right-hand side does not depend on anything: load it first
+      double own[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = (c0 + q < p) ? xr[c0 + q] : 0.0;
-      for (int32_t e = eb; e < ee; ++e) {
-        const double v = vals[e];
-        const double* xk = Xw + (int64_t)ci[e] * p + c0;
+      for (int q = 0; q < 8; ++q) own[q] = q < p ? xr[q] : 0.0;
+      wait_rows(W.flags, ci, eb, ee, W.epoch, W.ns_max);
+      fence_acquire();
+      for (int c0 = 0; c0 < p; c0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = c0 == 0 ? own[q] : ((c0 + q < p) ? xr[c0 + q] : 0.0);
+        for (int32_t e = eb; e < ee; ++e) {
+          const double v = vals[e];
+          const double* xk = Xw + (int64_t)ci[e] * p + c0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c0 + q < p) acc[q] = __dsub_rn(acc[q], __dmul_rn(v, __ldcg(xk + q)));
+        }
+        if (dval) {
+          const double d = dval[r];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __ddiv_rn(acc[q], d);
+        }
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (c0 + q < p) acc[q] = __dsub_rn(acc[q], __dmul_rn(v, __ldcg(xk + q)));
+          if (c0 + q < p) xr[c0 + q] = acc[q];
       }
-      if (dval) {
-        const double d = dval[r];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = __ddiv_rn(acc[q], d);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (c0 + q < p) xr[c0 + q] = acc[q];
+      st_release(W.flags + r, W.epoch);
     }
-    st_release(W.flags + r, W.epoch);
-    }
+    c = c_next;
   }
 }
 
@@ -224,8 +252,10 @@ static int64_t wave_grid(int32_t nchunks, int32_t width) {
   // Persistent warps, but only about two levels' worth of them: warps that
   // claim chunks further ahead only poll flags, and their acquire loads
   // compete with the rows being solved for L2 bandwidth.
-  int64_t g = (int64_t)sm_count() * 4;
-  const int64_t lvl = (2 * (int64_t)(width > 0 ? width : 1) + kWaveWarps - 1) / kWaveWarps;
+  static const int levels = getenv("RG_WAVE_LEVELS") ? atoi(getenv("RG_WAVE_LEVELS")) : 2;
+  static const int bps = getenv("RG_WAVE_BPS") ? atoi(getenv("RG_WAVE_BPS")) : 4;
+  int64_t g = (int64_t)sm_count() * bps;
+  const int64_t lvl = ((int64_t)levels * (width > 0 ? width : 1) + kWaveWarps - 1) / kWaveWarps;
   if (lvl < g) g = lvl;
   const int64_t need = ((int64_t)nchunks + kWaveWarps - 1) / kWaveWarps;
   if (need < g) g = need;
