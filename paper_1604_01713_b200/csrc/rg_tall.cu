@@ -920,6 +920,27 @@ __global__ void __launch_bounds__(W6 * 32, PM > 16 ? 1 : 2) tall_v6_kernel(TallP
     sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
     sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
   }
+  // two solves z R1^-1 R2^-1 become one with the upper-triangular R2 R1
+  // (CholQR2's final pass): half the dependent chain per row
+  const bool two = P.r1 && P.r2;
+  if (two) {
+    __syncthreads();
+    double* prod = wbase;  // the slab ring is free until the main loop
+    for (int e = threadIdx.x; e < PM * PM; e += (W6 * 32)) {
+      const int ii = e / PM, jj = e % PM;
+      double v = ii == jj ? 1.0 : 0.0;
+      if (ii < p && jj < p && ii <= jj) {
+        v = 0.0;
+        for (int k = ii; k <= jj; ++k) v = fma(P.r2[ii + (int64_t)k * p], P.r1[k + (int64_t)jj * p], v);
+        if (ii == jj) v = 1.0 / v;
+      } else if (ii > jj) {
+        v = 0.0;
+      }
+      prod[e] = v;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < PM * PM; e += (W6 * 32)) sR1[e] = prod[e];
+  }
   for (int k = threadIdx.x; k < L.total; k += (W6 * 32)) {
     const double* ptr;
     int64_t ld;
@@ -1109,7 +1130,7 @@ __global__ void __launch_bounds__(W6 * 32, PM > 16 ? 1 : 2) tall_v6_kernel(TallP
       for (int c = 0; c < PM; ++c) zr[c] = zt[c * kSS6 + lane];
       if (P.r1 || P.r2) {
         if (P.r1) trsm_row<PM>(zr, sR1, p);
-        if (P.r2) trsm_row<PM>(zr, sR2, p);
+        if (P.r2 && !two) trsm_row<PM>(zr, sR2, p);
 #pragma unroll
         for (int c = 0; c < PM; ++c) zt[c * kSS6 + lane] = zr[c];
       }
