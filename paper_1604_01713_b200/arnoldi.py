@@ -30,6 +30,12 @@ from .ortho import project_chain
 from .sparse_core import ShapeError
 
 
+# CGS2 against [C W] as one basis when C precedes W in the factorization's
+# allocation (three passes); False forces the reference's sequential C-then-W
+# order (five passes) -- tests compare the two
+JOINT_PROJECTION = True
+
+
 class ZeroStartBlock(ValueError):
     """The starting block is numerically zero (already converged)."""
 
@@ -267,7 +273,7 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     k_, w_ = fact.k, (m + 1) * L
     # [C W] as one basis when C sits in front of W (real data; the complex
     # tall pass has no aliased-term merge): 3 passes instead of 5
-    joint = (ortho == "cgs2" and C is not None and k_ > 0 and fact._c_src == C.data_ptr()
+    joint = (JOINT_PROJECTION and ortho == "cgs2" and C is not None and k_ > 0 and fact._c_src == C.data_ptr()
              and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
     if ortho == "cgs2" and joint:
         CW = fact._CW[:, : k_ + w_]

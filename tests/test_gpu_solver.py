@@ -196,3 +196,47 @@ def test_cfg4_family_64_sequence_matches_reference(cuda):
         hist = np.concatenate(rep.residual_history, axis=0)
         assert np.abs(hist - g[pre + "hist"]).max() <= 1e-8 * bnorm, i
         assert np.allclose(np.linalg.norm(rep.solution, axis=0), g[pre + "Xnorms"], rtol=1e-8)
+
+
+def test_joint_projection_matches_sequential_cgs2(cuda):
+    """CGS2 against [C W] as one basis (three passes) against the reference's
+    sequential C-then-W order (five passes): same H, F and basis to rounding,
+    same solver trajectory."""
+    from paper_1604_01713_b200 import arnoldi, problems
+    from paper_1604_01713_b200.recycling import RecycleSpace, prepare_cross_system
+    from paper_1604_01713_b200.solver import SolverConfig, _Operator, solve_sequence
+
+    A = problems.conv_diff_3d(24, 20.0)
+    n, L, k, m = A.n_rows, 8, 20, 10
+    rng = np.random.default_rng(5)
+    op = _Operator(A, None, "none")
+    rs = prepare_cross_system(RecycleSpace(u=rng.standard_normal((n, k)), c=None), op.apply)
+    C = rs.numpy()[1]
+    R0 = rng.standard_normal((n, L))
+    R0 -= C @ (C.T @ R0)
+    facts = {}
+    for joint in (True, False):
+        arnoldi.JOINT_PROJECTION = joint
+        try:
+            f = arnoldi.start(op.apply, R0, m_max=m, recycle=rs, seed=0)
+            for _ in range(m):
+                arnoldi.step(f, op.apply, recycle=rs)
+        finally:
+            arnoldi.JOINT_PROJECTION = True
+        facts[joint] = f
+    a, b = facts[True], facts[False]
+    scale = A.frobenius_norm()
+    assert np.abs(a.h_bar - b.h_bar).max() <= 1e-12 * scale
+    assert np.abs(a.f - b.f).max() <= 1e-12 * scale
+    assert np.abs(a.w_numpy() - b.w_numpy()).max() <= 1e-10
+    systems, kw = problems.cfg1_sequence()
+    runs = {}
+    for joint in (True, False):
+        arnoldi.JOINT_PROJECTION = joint
+        try:
+            runs[joint] = solve_sequence(systems, SolverConfig(**kw))
+        finally:
+            arnoldi.JOINT_PROJECTION = True
+    for r1, r2 in zip(runs[True], runs[False]):
+        assert r1.cycles == r2.cycles and r1.matvec_count == r2.matvec_count
+        assert np.abs(np.concatenate(r1.residual_history) - np.concatenate(r2.residual_history)).max() <= 1e-9
