@@ -41,6 +41,7 @@ import numpy as np  # noqa: E402
 
 P_BLOCK, K_RECYCLE, M_STEPS = 8, 20, 10
 SAMPLE_GRID = 64  # CPU sample: 64^3 rows of the same operator family
+DMMA_PEAK_TFLOPS = 36.7  # measured FP64 tensor (DMMA) throughput, profiles/microbench_r01.txt
 
 # operator families of the step workload: cfg4 (real conv-diff, BASELINE
 # configs[3]) and cfg5 (complex 27-point stencil, BASELINE configs[4])
@@ -300,10 +301,18 @@ def run_ours(args, rank, world):
     top_gbs = top[3] / (top[2] * 1e-3) / 1e9
     total_ms = sum(k[2] for k in kernels)
     traffic, traffic_src = _ncu_traffic(top[0], args.family)
+    top_flops = D.LaunchLog.flops.get(top[0], 0) if hasattr(D.LaunchLog, "flops") else 0
+    tensor = None
+    if top_flops:
+        per_launch_s = top[2] * 1e-3 / max(top[1], 1)
+        tensor = {"flops_per_launch": top_flops, "achieved_tflops": top_flops / per_launch_s / 1e12,
+                  "peak_tflops": DMMA_PEAK_TFLOPS, "frac": top_flops / per_launch_s / 1e12 / DMMA_PEAK_TFLOPS,
+                  "peak_source": "FP64 DMMA m8n8k4, tools/microbench.cu (profiles/microbench_r01.txt)"}
     roofline = {"bound": "hbm", "achieved": top_gbs, "peak": peak, "unit": "GB/s", "frac": top_gbs / peak,
                 "traffic": traffic, "traffic_source": traffic_src, "kernel": top[0],
                 "kernel_share": top[2] / max(total_ms, 1e-9),
-                "bytes_per_launch": top[3] // max(top[1], 1), "peak_source": peak_kind}
+                "bytes_per_launch": top[3] // max(top[1], 1), "peak_source": peak_kind,
+                "fp64_tensor": tensor}
 
     # end to end through the reference-facing call with host buffers
     e2e = None

@@ -203,6 +203,7 @@ class LaunchLog:
     count = 0
     timing = False
     records: list = []
+    flops: dict = {}  # label -> DMMA flops per launch (tall passes)
 
     @classmethod
     def reset(cls, timing: bool = False):
@@ -311,6 +312,10 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
                 + (p if zout is not None and (zin is None or zout.data_ptr() != zin.data_ptr()) else p if zout is not None else 0))
         label = (f"rg_tall p={p} in={int(zin is not None)} a={a1}+{a2} "
                  f"g{gmode}:{gc} trsm={int(r1 is not None) + int(r2 is not None)} out={int(zout is not None)}")
+        if LaunchLog.timing:
+            # tensor-core work: the update contraction and the Gram (4 real products per complex one)
+            contr = a1 + (0 if same_x else a2) + (gc if gmode in (1, 2) else 0)
+            LaunchLog.flops[label] = 2 * n * p * contr * (4 if cplx else 1)
         _t1(e0, label, esz * n * cols)
     if gout_k is not gout:
         gout.copy_(gout_k)
