@@ -1275,6 +1275,410 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
   return cudaGetLastError();
 }
 
+// ============================================================================
+// ws: warp-specialised stages for the CGS2 passes of the joint schedule.
+//
+// v6 keeps each warp's DRAM requests in a private 4-slab ring, so the bytes
+// in flight per SM fall whenever its warps are busy on DMMA chains or on
+// Gram slabs re-read from L2 (profiles/v6_study_r01.txt: P2 at 0.53 of the
+// HBM roof with the DMMA pipe 46% busy: the two barely overlap).  Here one
+// producer warp streams 64-row stages of every operand column into a
+// CTA-shared ring (one coalesced 512-byte column segment per warp cp.async;
+// each producer lane's completion lands on the stage's mbarrier through
+// cp.async.mbarrier.arrive.noinc), independent of what the consumers are
+// doing; eight consumer warps each own 8 rows of a stage and
+// run, from that one copy in shared memory,
+//   update   z += alpha * X S          (DMMA, S fragments in registers)
+//   store    Zout rows                 (optional)
+//   Gram     G += Gb^T z  or  z^T z    (DMMA; Gb may alias X: P2 of the
+//                                       joint schedule reads X once)
+// and release the stage with one mbarrier arrive per warp.  Column stride
+// 72 doubles (== 8 mod 16): the scalar update fragments and the 16-byte Gram
+// fragments (k mapped to row pairs) are bank-conflict free.  (A first cut
+// with one cp.async.bulk per column segment ran at 2.4 TB/s: ~50 cycles per
+// 512-byte bulk copy per SM.)
+// ============================================================================
+
+constexpr int kWsKS = 32;  // update k-steps (a1 <= 128)
+constexpr int kWsMaxStages = 6;
+constexpr size_t kWsSmemMax = 220 * 1024;
+
+#ifndef RG_WS_PROD8
+#define RG_WS_PROD8 2
+#endif
+// CW consumer warps x 8 rows per stage; column stride CW*8 + 8 doubles
+template <int CW>
+struct WsGeom {
+  static constexpr int kRows = CW * 8;
+  static constexpr int kS = kRows + 8;                 // == 8 mod 16
+  static constexpr int kProd = CW >= 6 ? RG_WS_PROD8 : 1;  // producer warps
+  static constexpr int kThreads = (CW + kProd) * 32;
+  static constexpr int kMinBlocks = CW >= 6 ? 1 : 2;
+  static constexpr size_t kSmemMax = CW >= 6 ? kWsSmemMax : 110 * 1024;
+  // <= 8 warps: two per SMSP, room for the update's S fragments in registers
+  static constexpr bool kBregOk = CW + kProd <= 8;
+};
+
+struct WsPlan {
+  int nslots, nload, x1slot0, gbslot0, stages, nz, a1, ngb;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WS_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @P1 bra WS_DONE;\n"
+      " bra WS_WAIT;\n"
+      "WS_DONE:\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// DMMA without `volatile`: the compiler may interleave independent chains
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+#ifndef RG_WS_NACC
+#define RG_WS_NACC 2
+#endif
+constexpr int kWsNacc = RG_WS_NACC;  // independent update accumulators (chain interleave)
+
+__device__ __forceinline__ void cp16_zfill(uint32_t dst, const void* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <int CW, int NT, int MT>
+__global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) tall_ws_kernel(TallParams P, WsPlan W) {
+  using G = WsGeom<CW>;
+  constexpr int kRows = G::kRows, kS = G::kS, kThreads = G::kThreads;
+  constexpr int MTA = MT > 0 ? MT : 1;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
+  __shared__ bool s_last;
+  const int p = P.p;
+  const int ks1 = (P.a1 + 3) / 4;
+  const size_t stage_words = (size_t)W.nslots * kS;
+  double* stage0 = smem;
+  double* sf1 = stage0 + (size_t)W.stages * stage_words;  // [ks1][NT][32]
+  double* red = stage0;  // [MTA][NT][64], reuses the ring after the main loop
+
+  for (size_t e = threadIdx.x; e < (size_t)W.stages * stage_words; e += kThreads) stage0[e] = 0.0;
+  for (int e = threadIdx.x; e < ks1 * NT * 32; e += kThreads) {
+    const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
+    const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
+    double v = 0.0;
+    if (aa < P.a1 && c < p) {
+      v = P.s1[aa + (int64_t)c * P.a1];
+      if (P.merge12) v = P.alpha1 * v + P.alpha2 * P.s2[aa + (int64_t)c * P.a2];
+    }
+    sf1[e] = v;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W.stages; ++s) {
+      mbar_init(&full[s], G::kProd * 32);
+      mbar_init(&empty[s], CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nunits = (P.n + kRows - 1) / kRows;
+  const int64_t my_units =
+      (int64_t)blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const bool gram_basis = MT > 0 && P.gmode == 1;
+  const bool gram_self = MT > 0 && P.gmode == 2;
+  const int mtiles = P.mtiles;
+
+  double acc[MTA][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MTA; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  if (warp >= CW) {
+    // ---------------- producers: lane t copies rows 2q, 2q + 1 (zero-filled
+    // past n) of columns jl, jl + kStep, ... of each operand segment; the
+    // source pointer and the slot offset advance by constants
+    constexpr int kCpc = kRows / 2;                  // 16-byte chunks per column
+    constexpr int kStep = G::kProd * 32 / kCpc;      // columns per producer pass
+    const int t = (warp - CW) * 32 + lane;
+    const int q = t % kCpc, jl = t / kCpc;
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t it = 0; it < my_units; ++it) {
+      if (it >= W.stages) mbar_wait(&empty[s], ph ^ 1u);
+      const int64_t row = ((int64_t)blockIdx.x + it * gridDim.x) * kRows + 2 * q;
+      const int64_t vr = P.n - row;
+      const int bytes = vr >= 2 ? 16 : (vr == 1 ? 8 : 0);
+      const int64_t off = bytes ? row : 0;
+      const uint32_t dq = smem_u32(stage0 + s * stage_words) + (uint32_t)(2 * q * 8);
+      auto segment = [&](const double* base, int64_t ld, int ncols, int slot0) {
+        const double* src = base + (int64_t)jl * ld + off;
+        uint32_t d = dq + (uint32_t)((slot0 + jl) * kS * 8);
+#pragma unroll 4
+        for (int j = jl; j < ncols; j += kStep) {
+          cp16_zfill(d, src, bytes);
+          src += kStep * ld;
+          d += kStep * kS * 8;
+        }
+      };
+      if (W.nz) segment(P.zin, P.ldzin, W.nz, 0);
+      if (W.a1) segment(P.x1, P.ldx1, W.a1, W.x1slot0);
+      if (W.ngb) segment(P.gb, P.ldgb, W.ngb, W.gbslot0);
+      cp_async_arrive_noinc(&full[s]);
+      if (++s == W.stages) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    cp_async_wait<0>();
+  } else {
+    // ---------------- consumers: warp owns stage rows rw .. rw + 7
+    const int mrow = lane >> 2, kq = lane & 3;
+    const int rw = warp * 8;
+    const bool upd = P.a1 > 0;
+    const bool wb = upd && (P.gmode != 0 || P.zout);
+    const double alpha = P.merge12 ? 1.0 : P.alpha1;
+    constexpr bool kBreg = G::kBregOk && NT == 1;
+    double bq[kBreg ? kWsKS : 1];
+    if (kBreg) {
+#pragma unroll
+      for (int ks = 0; ks < (kBreg ? kWsKS : 1); ++ks) bq[ks] = ks < ks1 ? sf1[ks * 32 + lane] : 0.0;
+    }
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t it = 0; it < my_units; ++it) {
+      mbar_wait(&full[s], ph);
+      double* st = stage0 + s * stage_words;
+      const int64_t r0 = ((int64_t)blockIdx.x + it * gridDim.x) * kRows;
+      double* zs = st;  // slots 0 .. NT*8-1
+      if (upd) {
+        double zf[NT][2], m[kWsNacc][NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            zf[nt][v] = zs[(nt * 8 + 2 * kq + v) * kS + rw + mrow];
+#pragma unroll
+            for (int q = 0; q < kWsNacc; ++q) m[q][nt][v] = 0.0;
+          }
+        const double* xs = st + W.x1slot0 * kS + kq * kS + rw + mrow;
+#pragma unroll
+        for (int ks = 0; ks < kWsKS; ++ks) {
+          if (ks < ks1) {
+            const double a = xs[ks * 4 * kS];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              dmma_nv(m[ks % kWsNacc][nt][0], m[ks % kWsNacc][nt][1], a,
+                      kBreg ? bq[kBreg ? ks : 0] : sf1[(ks * NT + nt) * 32 + lane]);
+          }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            double t = m[0][nt][v];
+#pragma unroll
+            for (int q = 1; q < kWsNacc; ++q) t += m[q][nt][v];
+            zf[nt][v] = zf[nt][v] + alpha * t;
+          }
+        if (wb) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) zs[(nt * 8 + 2 * kq + v) * kS + rw + mrow] = zf[nt][v];
+          __syncwarp();
+        }
+      }
+      if (P.zout) {
+#pragma unroll
+        for (int i = 0; i < NT * 2; ++i) {
+          const int e = lane + 32 * i, c = e >> 3, r = e & 7;
+          const int64_t row = r0 + rw + r;
+          if (c < p && row < P.n) P.zout[row + (int64_t)c * P.ldzout] = zs[c * kS + rw + r];
+        }
+      }
+      if (gram_basis || gram_self) {
+        double2 bz[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          bz[nt] = *reinterpret_cast<const double2*>(zs + (nt * 8 + mrow) * kS + rw + 2 * kq);
+        const double* gs = (gram_basis ? st + W.gbslot0 * kS : zs) + mrow * kS + rw + 2 * kq;
+        // all row tiles' first k-half, then the second: no back-to-back
+        // dependent DMMAs
+        double2 ga[MTA];
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          ga[mt] = mt < mtiles ? *reinterpret_cast<const double2*>(gs + mt * 8 * kS) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          if (mt < mtiles)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma_nv(acc[mt][nt][0], acc[mt][nt][1], ga[mt].x, bz[nt].x);
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          if (mt < mtiles)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma_nv(acc[mt][nt][0], acc[mt][nt][1], ga[mt].y, bz[nt].y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == W.stages) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+  }
+
+  // ---------------- epilogue: deterministic reductions (consumer-warp order)
+  __syncthreads();
+  if (gram_basis || gram_self) {
+    for (int ww = 0; ww < CW; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < MTA; ++mt)
+          if (mt < mtiles) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) {
+                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+                red[idx] = (ww == 0) ? acc[mt][nt][v] : red[idx] + acc[mt][nt][v];
+              }
+          }
+      }
+      __syncthreads();
+    }
+    const int ne = P.gc * p;
+    for (int e = threadIdx.x; e < ne; e += kThreads) {
+      const int gg = e % P.gc, c = e / P.gc;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = red[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = P.gc * p;
+  for (int e = threadIdx.x; e < ne; e += kThreads) {
+    double sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = sum;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+// the stage plan, or false when the pass is not a ws shape (triangular
+// solves, norms, two distinct terms, too many columns)
+template <int CW>
+static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem) {
+  using G = WsGeom<CW>;
+  if (P.r1 || P.r2 || P.gmode == 3) return false;
+  if (P.a2 > 0 && !P.merge12) return false;
+  if (P.a1 > 4 * kWsKS) return false;
+  if ((P.gmode == 1 || P.gmode == 2) && P.mtiles > MT) return false;
+  if (P.gmode == 2 && P.a1 == 0 && !P.zin) return false;
+  const int PM8 = NT * 8;
+  const bool alias = P.gmode == 1 && P.a1 > 0 && P.gb == P.x1 && P.ldgb == P.ldx1 && P.gc <= P.a1;
+  const int x1n = (P.a1 + 7) / 8 * 8;
+  const int gbn = (P.gmode == 1 && !alias) ? (P.gc + 7) / 8 * 8 : 0;
+  W.x1slot0 = PM8;
+  W.gbslot0 = alias ? PM8 : PM8 + x1n;
+  W.nslots = PM8 + x1n + gbn;
+  W.nz = P.zin ? P.p : 0;
+  W.a1 = P.a1;
+  W.ngb = (P.gmode == 1 && !alias) ? P.gc : 0;
+  W.nload = W.nz + P.a1 + W.ngb;
+  if (W.nload == 0) return false;
+  const size_t extra = (size_t)((P.a1 + 3) / 4) * NT * 32 * sizeof(double);
+  const size_t per_stage = (size_t)W.nslots * G::kS * sizeof(double);
+  const size_t red_bytes = (size_t)(MT > 0 ? MT : 1) * NT * 64 * sizeof(double);
+  int stages = kWsMaxStages;
+  while (stages >= 2 && (size_t)stages * per_stage + extra > G::kSmemMax) --stages;
+  if (stages < 2) return false;
+  static const int max_st = getenv("RG_WS_STAGES") ? atoi(getenv("RG_WS_STAGES")) : kWsMaxStages;
+  if (stages > max_st && max_st >= 2) stages = max_st;
+  if ((size_t)stages * per_stage < red_bytes) return false;
+  W.stages = stages;
+  smem = (size_t)stages * per_stage + extra;
+  return true;
+}
+
+template <int CW, int NT, int MT>
+static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, size_t smem, cudaStream_t st) {
+  using G = WsGeom<CW>;
+  auto k = tall_ws_kernel<CW, NT, MT>;
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmemMax);
+    per_sm = G::kMinBlocks;
+  }
+  const int64_t nunits = (P.n + G::kRows - 1) / G::kRows;
+  int64_t g = (int64_t)sm_count() * per_sm;
+  if (nunits < g) g = nunits;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, G::kThreads, smem, st>>>(P, W);
+  return cudaGetLastError();
+}
+
+template <int CW>
+static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cudaError_t& e) {
+  WsPlan W;
+  size_t smem = 0;
+  if (!ws_plan<CW>(P, NT, MT, W, smem)) return false;
+#define RG_WS_MT(NTv)                                                 \
+  switch (MT) {                                                       \
+    case 0: e = launch_ws<CW, NTv, 0>(P, W, smem, st); break;         \
+    case 2: e = launch_ws<CW, NTv, 2>(P, W, smem, st); break;         \
+    case 6: e = launch_ws<CW, NTv, 6>(P, W, smem, st); break;         \
+    case 13: e = launch_ws<CW, NTv, 13>(P, W, smem, st); break;       \
+    default: e = launch_ws<CW, NTv, 16>(P, W, smem, st); break;       \
+  }
+  if (NT == 1) {
+    RG_WS_MT(1)
+  } else {
+    RG_WS_MT(2)
+  }
+#undef RG_WS_MT
+  return true;
+}
+
+// returns false when the pass is not a ws shape (caller falls back to v6)
+static bool try_ws(const TallParams& P, int PM, cudaStream_t st, cudaError_t& e) {
+  static const int mode = getenv("RG_TALL_WS") ? atoi(getenv("RG_TALL_WS")) : 1;
+  if (!mode || PM > 16) return false;
+  const int NT = PM > 8 ? 2 : 1;
+  const int mt = (P.gmode == 1 || P.gmode == 2) ? P.mtiles : 0;
+  const int MT = mt == 0 ? 0 : (mt <= 2 ? 2 : (mt <= 6 ? 6 : (mt <= 13 ? 13 : 16)));
+  static const int cw = getenv("RG_WS_CW") ? atoi(getenv("RG_WS_CW")) : 8;
+  if (cw == 4) return try_ws_cw<4>(P, NT, MT, st, e);
+  if (cw == 6) return try_ws_cw<6>(P, NT, MT, st, e);
+  return try_ws_cw<8>(P, NT, MT, st, e);
+}
+
 // Passes without a basis Gram (update / store / self-Gram) run 4-warp CTAs
 // with an 8-deep slab ring; passes streaming a Gram basis keep 8 warps x 4
 // (profiles/v6_study_r01.txt: 2.97 -> 2.68 ms for the final CGS2 pass).
@@ -1489,6 +1893,13 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     if (which == 6 && ncol_slabs <= kMaxSlabs) {
       P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
+      if (!impl && try_ws(P, PM, st, e)) {
+        if (e != cudaSuccess) {
+          set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+          return RG_ECUDA;
+        }
+        return RG_OK;
+      }
       static const int wide_env = getenv("RG_V6_WIDE") ? atoi(getenv("RG_V6_WIDE")) : 1;
       const bool wide_ring = wide_env && gram_mode != 1 && PM <= 8 && P.mtiles <= 2 && !d_r1 && !d_r2 && a1 > 0;
       switch (PM) {

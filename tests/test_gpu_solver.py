@@ -239,4 +239,7 @@ def test_joint_projection_matches_sequential_cgs2(cuda):
             arnoldi.JOINT_PROJECTION = True
     for r1, r2 in zip(runs[True], runs[False]):
         assert r1.cycles == r2.cycles and r1.matvec_count == r2.matvec_count
-        assert np.abs(np.concatenate(r1.residual_history) - np.concatenate(r2.residual_history)).max() <= 1e-9
+        h1, h2 = np.concatenate(r1.residual_history), np.concatenate(r2.residual_history)
+        # rounding-level: the two schedules sum in different orders, and the
+        # recycled sequence carries the difference from system to system
+        assert np.abs(h1 - h2).max() <= 1e-9 * np.abs(h2).max()
