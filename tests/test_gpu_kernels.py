@@ -172,6 +172,35 @@ def test_tall_wide_terms_and_gram_split(cuda):
     assert _rel(out.cpu().numpy(), Gb.T @ ref) <= 1e-11
 
 
+@pytest.mark.parametrize("n", [5, 64, 1000, 70001])
+@pytest.mark.parametrize("p", [4, 8, 12, 16])
+def test_tall_joint_schedule_passes(cuda, n, p):
+    """The three passes of the joint [C W] projection (the warp-specialised
+    kernel's shapes): P1 Gram, P2 update + Gram against the same operand
+    (read once), P3 two merged terms over one operand + store (in place) +
+    self-Gram; basis widths up to 128 columns, ragged n."""
+    D = _dev()
+    rng = np.random.default_rng(n * 31 + p)
+    for w in (20, 100, 128):
+        X = rng.standard_normal((n, w))
+        Z = rng.standard_normal((n, p))
+        Xd, Zd = D.to_device_block(X), D.to_device_block(Z)
+        G1 = D.small(w, p)
+        D.tall(Zd, None, gram=("basis", Xd, G1))
+        g1 = X.T @ Z
+        assert _rel(G1.cpu().numpy(), g1) <= 1e-12
+        G2 = D.small(w, p)
+        D.tall(Zd, None, [(Xd, G1, -1.0)], gram=("basis", Xd, G2))
+        z1 = Z - X @ G1.cpu().numpy()
+        # n-term sums of |X||z1|-sized products: bound the error by n * 100 eps
+        assert np.abs(G2.cpu().numpy() - X.T @ z1).max() <= 1e-14 * n * np.abs(X).max() * np.abs(z1).max()
+        Gs = D.small(p, p)
+        D.tall(Zd, Zd, [(Xd, G1, -1.0), (Xd, G2, -1.0)], gram=("self", Gs))
+        z2 = (Z - X @ G1.cpu().numpy()) - X @ G2.cpu().numpy()
+        assert _rel(D.to_numpy_block(Zd), z2) <= 1e-12
+        assert _rel(Gs.cpu().numpy(), z2.T @ z2) <= 1e-12
+
+
 def test_tall_empty_rows(cuda):
     D = _dev()
     out = D.small(3, 2)
