@@ -1361,7 +1361,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 
-template <int CW, int NT, int MT>
+template <int CW, int NT, int MT, int KSR = 0>
 __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) tall_ws_kernel(TallParams P, WsPlan W) {
   using G = WsGeom<CW>;
   constexpr int kRows = G::kRows, kS = G::kS, kThreads = G::kThreads;
@@ -1454,11 +1454,14 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
     const bool upd = P.a1 > 0;
     const bool wb = upd && (P.gmode != 0 || P.zout);
     const double alpha = P.merge12 ? 1.0 : P.alpha1;
-    constexpr bool kBreg = G::kBregOk && NT == 1;
-    double bq[kBreg ? kWsKS : 1];
+    // KSR > 0: the update's S fragments (a1 <= 4*KSR, NT == 1) live in
+    // registers -- a fifth of the pass's shared-memory wavefronts
+    constexpr bool kBreg = KSR > 0 && NT == 1;
+    constexpr int kKS = kBreg ? KSR : kWsKS;
+    double bq[kBreg ? KSR : 1];
     if (kBreg) {
 #pragma unroll
-      for (int ks = 0; ks < (kBreg ? kWsKS : 1); ++ks) bq[ks] = ks < ks1 ? sf1[ks * 32 + lane] : 0.0;
+      for (int ks = 0; ks < (kBreg ? KSR : 1); ++ks) bq[ks] = ks < ks1 ? sf1[ks * 32 + lane] : 0.0;
     }
     int s = 0;
     unsigned ph = 0;
@@ -1479,7 +1482,7 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
           }
         const double* xs = st + W.x1slot0 * kS + kq * kS + rw + mrow;
 #pragma unroll
-        for (int ks = 0; ks < kWsKS; ++ks) {
+        for (int ks = 0; ks < kKS; ++ks) {
           if (ks < ks1) {
             const double a = xs[ks * 4 * kS];
 #pragma unroll
@@ -1627,10 +1630,10 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   return true;
 }
 
-template <int CW, int NT, int MT>
+template <int CW, int NT, int MT, int KSR = 0>
 static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, size_t smem, cudaStream_t st) {
   using G = WsGeom<CW>;
-  auto k = tall_ws_kernel<CW, NT, MT>;
+  auto k = tall_ws_kernel<CW, NT, MT, KSR>;
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmemMax);
@@ -1657,7 +1660,12 @@ static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cuda
     case 13: e = launch_ws<CW, NTv, 13>(P, W, smem, st); break;       \
     default: e = launch_ws<CW, NTv, 16>(P, W, smem, st); break;       \
   }
-  if (NT == 1) {
+  static const int breg = getenv("RG_WS_BREG") ? atoi(getenv("RG_WS_BREG")) : 1;
+  if (NT == 1 && breg && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13) {
+    // the joint schedule's P2 shape at p <= 8: S in registers (3.08 -> 3.00-3.05
+    // ms at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
+    e = launch_ws<CW, 1, 13, 26>(P, W, smem, st);
+  } else if (NT == 1) {
     RG_WS_MT(1)
   } else {
     RG_WS_MT(2)
