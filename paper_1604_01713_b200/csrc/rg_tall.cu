@@ -1300,7 +1300,7 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
 // ============================================================================
 
 constexpr int kWsKS = 32;  // update k-steps (a1 <= 128)
-constexpr int kWsMaxStages = 6;
+constexpr int kWsMaxStages = 8;
 constexpr size_t kWsSmemMax = 220 * 1024;
 
 #ifndef RG_WS_PROD8
@@ -1374,7 +1374,10 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
   const size_t stage_words = (size_t)W.nslots * kS;
   double* stage0 = smem;
   double* sf1 = stage0 + (size_t)W.stages * stage_words;  // [ks1][NT][32]
+  double* sR = sf1 + (size_t)ks1 * NT * 32;                // [NT*8][NT*8] solve factor
   double* red = stage0;  // [MTA][NT][64], reuses the ring after the main loop
+  constexpr int PM8 = NT * 8;
+  const bool trsm = KSR == 0 && (P.r1 || P.r2);  // the KSR variants never carry solves
 
   for (size_t e = threadIdx.x; e < (size_t)W.stages * stage_words; e += kThreads) stage0[e] = 0.0;
   for (int e = threadIdx.x; e < ks1 * NT * 32; e += kThreads) {
@@ -1386,6 +1389,25 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
       if (P.merge12) v = P.alpha1 * v + P.alpha2 * P.s2[aa + (int64_t)c * P.a2];
     }
     sf1[e] = v;
+  }
+  if (trsm) {
+    // z R1^-1 [R2^-1] as one solve with R (= R1, or the upper-triangular R2 R1),
+    // row-major, reciprocal diagonal (as v6)
+    for (int e = threadIdx.x; e < PM8 * PM8; e += kThreads) {
+      const int ii = e / PM8, jj = e % PM8;
+      double v = ii == jj ? 1.0 : 0.0;
+      if (ii < p && jj < p && ii <= jj) {
+        if (P.r1 && P.r2) {
+          v = 0.0;
+          for (int k = ii; k <= jj; ++k) v = fma(P.r2[ii + (int64_t)k * p], P.r1[k + (int64_t)jj * p], v);
+        } else {
+          const double* r = P.r1 ? P.r1 : P.r2;
+          v = r[ii + (int64_t)jj * p];
+        }
+        if (ii == jj) v = 1.0 / v;
+      }
+      sR[e] = v;
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < W.stages; ++s) {
@@ -1452,7 +1474,7 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
     const int mrow = lane >> 2, kq = lane & 3;
     const int rw = warp * 8;
     const bool upd = P.a1 > 0;
-    const bool wb = upd && (P.gmode != 0 || P.zout);
+    const bool wb = upd && (P.gmode != 0 || P.zout || trsm);
     const double alpha = P.merge12 ? 1.0 : P.alpha1;
     // KSR > 0: the update's S fragments (a1 <= 4*KSR, NT == 1) live in
     // registers -- a fifth of the pass's shared-memory wavefronts
@@ -1507,6 +1529,18 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
             for (int v = 0; v < 2; ++v) zs[(nt * 8 + 2 * kq + v) * kS + rw + mrow] = zf[nt][v];
           __syncwarp();
         }
+      }
+      if (trsm) {
+        // one lane per row of this warp's 8 rows
+        if (lane < 8) {
+          double zr[PM8];
+#pragma unroll
+          for (int c = 0; c < PM8; ++c) zr[c] = zs[c * kS + rw + lane];
+          trsm_row<PM8>(zr, sR, p);
+#pragma unroll
+          for (int c = 0; c < PM8; ++c) zs[c * kS + rw + lane] = zr[c];
+        }
+        __syncwarp();
       }
       if (P.zout) {
 #pragma unroll
@@ -1599,7 +1633,7 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
 template <int CW>
 static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem) {
   using G = WsGeom<CW>;
-  if (P.r1 || P.r2 || P.gmode == 3) return false;
+  if (P.gmode == 3) return false;
   if (P.a2 > 0 && !P.merge12) return false;
   if (P.a1 > 4 * kWsKS) return false;
   if ((P.gmode == 1 || P.gmode == 2) && P.mtiles > MT) return false;
@@ -1616,7 +1650,7 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   W.ngb = (P.gmode == 1 && !alias) ? P.gc : 0;
   W.nload = W.nz + P.a1 + W.ngb;
   if (W.nload == 0) return false;
-  const size_t extra = (size_t)((P.a1 + 3) / 4) * NT * 32 * sizeof(double);
+  const size_t extra = ((size_t)((P.a1 + 3) / 4) * NT * 32 + (size_t)PM8 * PM8) * sizeof(double);
   const size_t per_stage = (size_t)W.nslots * G::kS * sizeof(double);
   const size_t red_bytes = (size_t)(MT > 0 ? MT : 1) * NT * 64 * sizeof(double);
   int stages = kWsMaxStages;
@@ -1625,6 +1659,14 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   static const int max_st = getenv("RG_WS_STAGES") ? atoi(getenv("RG_WS_STAGES")) : kWsMaxStages;
   if (stages > max_st && max_st >= 2) stages = max_st;
   if ((size_t)stages * per_stage < red_bytes) return false;
+  // narrow passes (the CholQR solves: 8 columns, 4.6 KB stages) cannot keep
+  // enough bytes in flight per SM through a ring of whole stages -- v3 / v6
+  // serve them (1.15-1.2 ms vs 0.33-0.39 ms per cfg4 pass when forced here)
+  if ((size_t)stages * per_stage < (size_t)96 * 1024) return false;
+  // below ~64 streamed columns the fixed per-stage cost (mbarrier round
+  // trips, 64-row stages) loses to v6 (tools/ws_sweep.py, profiles/ws_study_r01.txt)
+  static const int min_cols = getenv("RG_WS_MIN_COLS") ? atoi(getenv("RG_WS_MIN_COLS")) : 64;
+  if (W.nload < min_cols) return false;
   W.stages = stages;
   smem = (size_t)stages * per_stage + extra;
   return true;
@@ -1661,7 +1703,7 @@ static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cuda
     default: e = launch_ws<CW, NTv, 16>(P, W, smem, st); break;       \
   }
   static const int breg = getenv("RG_WS_BREG") ? atoi(getenv("RG_WS_BREG")) : 1;
-  if (NT == 1 && breg && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13) {
+  if (NT == 1 && breg && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
     // the joint schedule's P2 shape at p <= 8: S in registers (3.08 -> 3.00-3.05
     // ms at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
     e = launch_ws<CW, 1, 13, 26>(P, W, smem, st);
@@ -1889,6 +1931,15 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
     // measured per pass type (profiles/ab_tall_r01.txt): v6 for passes with
     // an update term or a triangular-solve store, v5 for a pure basis Gram,
     // v3 for the self-Gram solve pass of CholQR2
+    P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
+    if (!impl && try_ws(P, PM, st, e)) {
+      if (e != cudaSuccess) {
+        set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+        return RG_ECUDA;
+      }
+      return RG_OK;
+    }
+    P.merge12 = 0;
     int which = 6;
     if (a1 + a2 == 0) {
       if (gram_mode == 1)
@@ -1901,13 +1952,6 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     if (which == 6 && ncol_slabs <= kMaxSlabs) {
       P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
-      if (!impl && try_ws(P, PM, st, e)) {
-        if (e != cudaSuccess) {
-          set_error("rg_tall_f64: %s", cudaGetErrorString(e));
-          return RG_ECUDA;
-        }
-        return RG_OK;
-      }
       static const int wide_env = getenv("RG_V6_WIDE") ? atoi(getenv("RG_V6_WIDE")) : 1;
       const bool wide_ring = wide_env && gram_mode != 1 && PM <= 8 && P.mtiles <= 2 && !d_r1 && !d_r2 && a1 > 0;
       switch (PM) {
