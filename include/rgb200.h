@@ -80,6 +80,14 @@ int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_end,
  *
  * S1/S2/R1/R2 and Gout are DEVICE arrays, column-major with ld = rows.
  * Gram sums are reduced in a fixed order (deterministic run to run).
+ * When Gb aliases X1 (same pointer and ld, gc <= a1), and when X1 == X2
+ * with a1 == a2, the operand is streamed once.
+ *
+ * Implementation: passes streaming >= 64 columns without norms run the
+ * warp-specialised kernel (producer warps fill a CTA-shared ring of 64-row
+ * stages, consumer warps run the DMMA update / Gram from it); narrower
+ * passes, norms and p > 16 run the per-warp slab-ring kernel (v6, v5, v3).
+ * RG_TALL_WS=0 in the environment forces the latter (A/B runs).
  *
  * Replaces the numpy/OpenBLAS products of the hot path:
  *   arnoldi.step CGS2 branch   arnoldi.py:172-180   (C^T Ahat, Ahat -= C S,
