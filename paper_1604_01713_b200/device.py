@@ -12,6 +12,8 @@ from __future__ import annotations
 
 import ctypes
 
+import os
+
 import numpy as np
 import torch
 
@@ -173,13 +175,35 @@ def ptr(t: torch.Tensor | None) -> int | None:
 class Workspace:
     """Per-device scratch buffer; the leading 256 bytes hold the ticket
     counter of rg_tall's last-CTA reduction (zeroed once, re-armed by the
-    kernels)."""
+    kernels).
+
+    RG_WS_GUARD=<bytes> (debug): every request gets a fresh buffer of exactly
+    the requested size followed by a guard region; ``check`` after each
+    launch raises if a kernel wrote past its workspace."""
 
     _pools: dict = {}
+    _guard = int(os.environ.get("RG_WS_GUARD", "0"))
+    _last = None
+
+    @classmethod
+    def check(cls, label: str) -> None:
+        if not cls._guard or cls._last is None:
+            return
+        buf, nb = cls._last
+        torch.cuda.synchronize(buf.device)
+        if not bool((buf[nb:] == 0xA5).all()):
+            bad = int((buf[nb:] != 0xA5).nonzero()[-1].item()) + 1
+            raise RuntimeError(f"workspace overflow after {label}: {bad} bytes past the {nb}-byte request")
 
     @classmethod
     def get(cls, nbytes: int, device=None, slot: int = 0) -> torch.Tensor:
         dev = require_cuda(device)
+        if cls._guard:
+            nb = max(int(nbytes), 256)
+            buf = torch.zeros(nb + cls._guard, dtype=torch.uint8, device=dev)
+            buf[nb:] = 0xA5
+            cls._last = (buf, nb)
+            return buf[:nb]
         key = (dev.index, slot)
         buf = cls._pools.get(key)
         if buf is None or buf.numel() < nbytes:
@@ -301,6 +325,7 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
             ptr(gb), ld_of(gb) if gb is not None else 1, gc, ptr(gout_k),
             ptr(ws), ws.numel() if ws is not None else 0, stream_ptr())
     _lib.check(rc, "tall")
+    Workspace.check(f"rg_tall n={n} p={p} a={a1}+{a2} gmode={gmode} gc={gc} cplx={cplx}")
     if n > 0 or gmode:
         esz = 16 if cplx else 8
         # a Gram basis that aliases an update operand is streamed once
@@ -508,6 +533,7 @@ def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1) -> None:
     rc = L.rg_cgs2_f64(n, p, Z.data_ptr(), ld_of(Z), ptr(C), ld_of(C) if C is not None else 1, k,
                        W.data_ptr(), ld_of(W), w, coef.data_ptr(), ptr(G1), ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check(rc, "cgs2")
+    Workspace.check(f"rg_cgs2 n={n} p={p} k={k} w={w}")
     joint = (k and w and ld_of(C) == ld_of(W) and W.data_ptr() == C.data_ptr() + k * ld_of(C) * C.element_size()
              and k + w <= MAX_GC)
     LaunchLog.count += 3 if joint else (2 if k else 0) + (2 if w else 0) + 1
@@ -520,6 +546,7 @@ def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch
     rc = L.rg_cholqr2_f64(n, p, X.data_ptr(), ld_of(X), Q.data_ptr(), ld_of(Q), small.data_ptr(), status.data_ptr(),
                           1 if gram_ready else 0, ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check(rc, "cholqr2")
+    Workspace.check(f"rg_cholqr2 n={n} p={p}")
     LaunchLog.count += 4 + (0 if gram_ready else 1)
 
 
