@@ -201,6 +201,40 @@ def test_tall_joint_schedule_passes(cuda, n, p):
         assert _rel(Gs.cpu().numpy(), z2.T @ z2) <= 1e-12
 
 
+def test_tall_passes_ignore_padding_rows(cuda):
+    """Blocks whose leading-dimension padding (rows n .. ld-1) and spare
+    columns hold NaN: every pass shape (v6 and warp-specialised) reads only
+    the n logical rows (tools/pad_poison.py runs the wider sweep)."""
+    D = _dev()
+    rng = np.random.default_rng(77)
+
+    def poisoned(a, extra=8):
+        a = np.asfortranarray(a)
+        store = torch.full((a.shape[1] + extra, D.round_ld(a.shape[0])), float("nan"), dtype=torch.float64,
+                           device=cuda)
+        v = store.t()[: a.shape[0], : a.shape[1]]
+        v.copy_(torch.from_numpy(a.T).t())
+        return v
+
+    for n in (1000, 70001):
+        p = 8
+        for a1, gmode, alias in ((100, 1, True), (28, 1, False), (20, 0, False), (100, 2, False)):
+            X, Z, Gb = rng.standard_normal((n, a1)), rng.standard_normal((n, p)), rng.standard_normal((n, 40))
+            S = rng.standard_normal((a1, p))
+            Sd = D.small(a1, p)
+            Sd.copy_(torch.from_numpy(S))
+            Xd, Gd, Zo = poisoned(X), poisoned(Gb), poisoned(np.zeros((n, p)))
+            gb = (Xd if alias else Gd) if gmode == 1 else None
+            G = D.small(gb.shape[1] if gmode == 1 else p, p) if gmode else None
+            gram = None if not gmode else (("basis", gb, G) if gmode == 1 else ("self", G))
+            D.tall(poisoned(Z), Zo, [(Xd, Sd, -1.0)], gram=gram)
+            z = Z - X @ S
+            assert _rel(D.to_numpy_block(Zo), z) <= 1e-12
+            if gmode:
+                ref = (X if alias else Gb).T @ z if gmode == 1 else z.T @ z
+                assert np.isfinite(G.cpu().numpy()).all() and _rel(G.cpu().numpy(), ref) <= 1e-11
+
+
 def test_tall_empty_rows(cuda):
     D = _dev()
     out = D.small(3, 2)
