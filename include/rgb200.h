@@ -144,15 +144,17 @@ int64_t rg_tsqr_workspace_bytes(int64_t n, int32_t p);
  * column-major (F = S1 + S2, H = c1 + c2 on the host, arnoldi.py:177,180);
  * if d_gram is non-NULL it receives Z^T Z of the projected block (the first
  * CholQR Gram).  p <= 16, k + w <= 256.
- * When W directly follows C in one allocation (d_w == d_c + k*ldc, ldw ==
- * ldc) and k + w <= 128, the projection runs against [C W] as one basis in
- * three passes (C is orthogonal to W: the same CGS2 up to rounding) and
- * d_coef holds G1 = [S1; c1] | G2 = [S2; c2], each (k+w) x p.
+ * joint != 0 (the solver's layout: W directly follows C in one allocation,
+ * d_w == d_c + k*ldc, ldw == ldc, k + w <= 128, and C is orthogonal to W)
+ * runs the projection against [C W] as one basis in three passes -- the
+ * same CGS2 up to rounding -- and d_coef holds G1 = [S1; c1] | G2 =
+ * [S2; c2], each (k+w) x p; the workspace must then cover gc = k + w.
+ * joint == 0 always runs the sequential schedule (any C, W).
  */
 int rg_cgs2_f64(int64_t n, int32_t p, double* d_z, int64_t ldz,
                 const double* d_c, int64_t ldc, int32_t k,
                 const double* d_w, int64_t ldw, int32_t w,
-                double* d_coef, double* d_gram,
+                double* d_coef, double* d_gram, int32_t joint,
                 void* d_work, int64_t work_bytes, void* stream);
 
 /*

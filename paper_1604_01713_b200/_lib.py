@@ -37,7 +37,7 @@ PROTOTYPES = {
     "rg_tsqr_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "rg_tsqr_workspace_bytes": (c_i64, [c_i64, c_i32]),
     "rg_cgs2_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr, c_i64, c_i32,
-                                   c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
+                                   c_ptr, c_ptr, c_i32, c_ptr, c_i64, c_ptr]),
     "rg_cholqr2_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i32,
                                       c_ptr, c_i64, c_ptr]),
     "rg_spmm_csr_c128": (ctypes.c_int, [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64,

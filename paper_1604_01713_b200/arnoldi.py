@@ -278,8 +278,8 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     if ortho == "cgs2" and joint:
         CW = fact._CW[:, : k_ + w_]
         if _dev.fused_ok() and L <= _dev.MAX_P_FUSED:
-            # rg_cgs2_f64 sees C and W adjacent and runs the same three passes
-            _dev.cgs2(Ahat, fact._CW[:, :k_], active, fact._coef, scr.G1)
+            # rg_cgs2_f64 runs the same three passes on the adjacent [C W]
+            _dev.cgs2(Ahat, fact._CW[:, :k_], active, fact._coef, scr.G1, joint=True)
         else:
             kw = k_ + w_
             G1 = fact._coef[: kw * L].view(L, kw).t()

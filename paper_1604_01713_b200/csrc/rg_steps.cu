@@ -41,16 +41,22 @@ int tall_call(int64_t n, int32_t p, const double* zin, int64_t ldzin, double* zo
 
 extern "C" int rg_cgs2_f64(int64_t n, int32_t p, double* d_z, int64_t ldz, const double* d_c, int64_t ldc,
                            int32_t k, const double* d_w, int64_t ldw, int32_t w, double* d_coef, double* d_gram,
-                           void* d_work, int64_t work_bytes, void* stream) {
+                           int32_t joint, void* d_work, int64_t work_bytes, void* stream) {
   using namespace rg;
   clear_error();
   RG_REQUIRE(n >= 0 && p >= 1 && p <= 16, "rg_cgs2_f64: p=%d outside [1, 16]", p);
   RG_REQUIRE(k >= 0 && w >= 0 && (k == 0 || d_c) && (w == 0 || d_w) && d_z && d_coef,
              "rg_cgs2_f64: bad operands");
   RG_REQUIRE(k + w <= 256, "rg_cgs2_f64: k + w = %d too wide for one schedule", k + w);
-  if (k > 0 && w > 0 && d_w == d_c + (int64_t)k * ldc && ldw == ldc && k + w <= 128) {
-    // C and W adjacent in one allocation: project against [C W] as one basis
-    // (C is orthogonal to W, so this is the same CGS2 up to rounding):
+  // the joint schedule is the caller's explicit choice: adjacency alone can
+  // be a coincidence of the allocator, and the schedule assumes C is
+  // orthogonal to W (the solver's invariant, not every caller's)
+  RG_REQUIRE(!joint || (k > 0 && w > 0 && d_w == d_c + (int64_t)k * ldc && ldw == ldc && k + w <= 128),
+             "rg_cgs2_f64: joint schedule needs W directly after C in one allocation (d_w == d_c + k*ldc, "
+             "ldw == ldc) and k + w <= 128");
+  if (joint) {
+    // project against [C W] as one basis (C is orthogonal to W, so this is
+    // the same CGS2 up to rounding):
     //   P1  G1 = [C W]^T z
     //   P2  G2 = [C W]^T (z - [C W] G1)
     //   P3  z <- z - [C W] (G1 + G2)  (aliased terms merged), self Gram

@@ -522,20 +522,21 @@ def fused_ok() -> bool:
     return _COMM is None and not LaunchLog.timing
 
 
-def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1) -> None:
+def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1, joint: bool = False) -> None:
     """One call: CGS2 of Z against C then W (twice) in place; coef receives
-    S1|c1|S2|c2; G1 (optional) receives Z^T Z of the result."""
+    S1|c1|S2|c2; G1 (optional) receives Z^T Z of the result.  ``joint``:
+    W follows C in one allocation and C is orthogonal to W -- three passes
+    against [C W], coef = G1|G2 (rg_cgs2_f64)."""
     L = lib()
     n, p = Z.shape
     k = 0 if C is None else C.shape[1]
     w = W.shape[1]
     ws = Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k + w, p)))
     rc = L.rg_cgs2_f64(n, p, Z.data_ptr(), ld_of(Z), ptr(C), ld_of(C) if C is not None else 1, k,
-                       W.data_ptr(), ld_of(W), w, coef.data_ptr(), ptr(G1), ws.data_ptr(), ws.numel(), stream_ptr())
+                       W.data_ptr(), ld_of(W), w, coef.data_ptr(), ptr(G1), 1 if joint else 0, ws.data_ptr(),
+                       ws.numel(), stream_ptr())
     _lib.check(rc, "cgs2")
     Workspace.check(f"rg_cgs2 n={n} p={p} k={k} w={w}")
-    joint = (k and w and ld_of(C) == ld_of(W) and W.data_ptr() == C.data_ptr() + k * ld_of(C) * C.element_size()
-             and k + w <= MAX_GC)
     LaunchLog.count += 3 if joint else (2 if k else 0) + (2 if w else 0) + 1
 
 

@@ -362,8 +362,10 @@ def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
     coef = torch.zeros((2 * k + 2 * w) * p, dtype=torch.float64, device=cuda)
     small = torch.zeros(4 * p * p, dtype=torch.float64, device=cuda)
     ws = D.Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, max(k, w)))
+    # joint = 0: the sequential schedule, whatever the allocator placed where
+    # (W directly after C by coincidence must not switch schedules)
     rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), Cd.data_ptr(), D.ld_of(Cd), k, Wd.data_ptr(), D.ld_of(Wd), w,
-                       coef.data_ptr(), small.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+                       coef.data_ptr(), small.data_ptr(), 0, ws.data_ptr(), ws.numel(), D.stream_ptr())
     assert rc == 0
     hc = coef.cpu().numpy()
     S1 = hc[:k * p].reshape(p, k).T
@@ -383,3 +385,35 @@ def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
     q_ref, r_ref, _ = oracle.reduced_qr(ref)
     assert _rel(R, r_ref) <= 1e-11
     assert np.abs(D.to_numpy_block(Qd) - q_ref).max() <= 1e-10
+
+
+def test_c_abi_cgs2_joint_schedule(cuda):
+    """rg_cgs2_f64 with joint = 1 (the solver's layout: W follows C in one
+    allocation, C orthogonal to W) equals the sequential schedule to rounding;
+    joint = 1 on operands that are not adjacent is rejected."""
+    from paper_1604_01713_b200 import _lib
+    from paper_1604_01713_b200 import device as D
+
+    L = _lib.load()
+    rng = np.random.default_rng(22)
+    n, p, k, w = 40_000, 8, 20, 60
+    Q = np.linalg.qr(rng.standard_normal((n, k + w)))[0]
+    A = rng.standard_normal((n, p))
+    ref, F, H = oracle.cgs2_project(A, Q[:, :k], Q[:, k:])
+    CW = D.to_device_block(Q)
+    ws = D.Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, k + w))
+    coef = torch.zeros(2 * (k + w) * p, dtype=torch.float64, device=cuda)
+    Zd = D.to_device_block(A)
+    rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), CW.data_ptr(), D.ld_of(CW), k, CW[:, k:].data_ptr(),
+                       D.ld_of(CW), w, coef.data_ptr(), None, 1, ws.data_ptr(), ws.numel(), D.stream_ptr())
+    assert rc == 0
+    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12 * 1e3
+    hc = coef.cpu().numpy()
+    G1 = hc[: (k + w) * p].reshape(p, k + w).T
+    G2 = hc[(k + w) * p:].reshape(p, k + w).T
+    assert np.abs((G1 + G2)[:k] - F).max() <= 1e-11 * max(1.0, np.abs(F).max())
+    assert np.abs((G1 + G2)[k:] - H).max() <= 1e-11 * max(1.0, np.abs(H).max())
+    Wsep = D.to_device_block(Q[:, k:])
+    rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), CW.data_ptr(), D.ld_of(CW), k, Wsep.data_ptr(),
+                       D.ld_of(Wsep), w, coef.data_ptr(), None, 1, ws.data_ptr(), ws.numel(), D.stream_ptr())
+    assert rc == _lib.RG_EBADARG

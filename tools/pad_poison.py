@@ -89,7 +89,7 @@ def main():
             sm = torch.zeros(4 * p * p, dtype=torch.float64, device=dev)
             ws = D.Workspace.get(L.rg_tall_workspace_bytes(n, p, k, w, 1, k + w))
             rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), Cd.data_ptr(), D.ld_of(Cd), k, Wd.data_ptr(),
-                               D.ld_of(Wd), w, coef.data_ptr(), sm.data_ptr(), ws.data_ptr(), ws.numel(),
+                               D.ld_of(Wd), w, coef.data_ptr(), sm.data_ptr(), 1 if joint else 0, ws.data_ptr(), ws.numel(),
                                D.stream_ptr())
             torch.cuda.synchronize()
             z = A - C @ (C.T @ A) - W @ (W.T @ A)
