@@ -330,10 +330,19 @@ __global__ void __launch_bounds__(kTallThreads, 1) tall_kernel(TallParams P) {
 
 constexpr int kV3Warps = 8;
 constexpr int kV3Threads = kV3Warps * 32;
+#ifndef RG_V3_NARROW_BLOCKS
+#define RG_V3_NARROW_BLOCKS 3
+#endif
 constexpr int kSlabStride = 36;  // 32 rows + 4: conflict-free fragment reads
 
+// the narrow CholQR solve + self-Gram pass (p <= 8, <= 2 Gram tiles) is
+// latency-bound: 3 CTAs per SM instead of 2
 template <int PM, int MTMAX>
-__global__ void __launch_bounds__(kV3Threads, 2) tall_v3_kernel(TallParams P) {
+struct V3MinBlocks {
+  static constexpr int value = (PM <= 8 && MTMAX <= 2) ? RG_V3_NARROW_BLOCKS : 2;
+};
+template <int PM, int MTMAX>
+__global__ void __launch_bounds__(kV3Threads, (V3MinBlocks<PM, MTMAX>::value)) tall_v3_kernel(TallParams P) {
   constexpr int PM8 = PM < 8 ? 8 : PM;
   constexpr int NT = PM8 / 8;
   extern __shared__ __align__(16) double smem[];
@@ -1779,7 +1788,7 @@ static cudaError_t launch_v3(const TallParams& P, int64_t max_grid, cudaStream_t
 #define RG_V3_CASE(PMv)                                                                   \
   case PMv:                                                                               \
     switch (mtmax) {                                                                      \
-      case 2: e = launch_v3<PMv, 2>(P, bound, st); break;                                 \
+      case 2: e = launch_v3<PMv, 2>(P, tall_grid_bound(), st); break;                     \
       case 6: e = launch_v3<PMv, 6>(P, bound, st); break;                                 \
       case 12: e = launch_v3<PMv, 12>(P, bound, st); break;                               \
       default: e = launch_v3<PMv, 16>(P, bound, st); break;                               \
@@ -1826,8 +1835,10 @@ static bool aligned16(const void* p, int64_t ld) {
   return p == nullptr || (((uintptr_t)p & 15u) == 0 && (ld & 1) == 0);
 }
 
-// upper bound on the grid of any rg_tall launch (workspace sizing)
-static int64_t tall_grid_bound() { return (int64_t)sm_count() * 2; }
+// upper bound on the grid of any rg_tall launch (workspace sizing): the
+// narrow v3 pass runs up to 3 CTAs per SM, everything else at most 2
+static int64_t tall_grid_bound() { return (int64_t)sm_count() * 4; }
+static int64_t tall_grid_bound2() { return (int64_t)sm_count() * 2; }
 
 #define RG_TALL_CASE(PMv)                                                                 \
   case PMv:                                                                               \
@@ -1897,7 +1908,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const int mtmax = pick_mtmax(P.mtiles);
   const size_t smem = tall_smem(PM, a1, a2, d_r1 != nullptr, d_r2 != nullptr, gram_mode, mtmax);
   RG_REQUIRE(smem <= 200 * 1024, "rg_tall_f64: %zu bytes of shared memory (terms too wide)", smem);
-  const int64_t bound = tall_grid_bound();
+  const int64_t bound = tall_grid_bound2();
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   const bool aligned = aligned16(P.zin, P.ldzin) && aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) &&
