@@ -1957,6 +1957,8 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
         which = P.mtiles > 12 ? 6 : 5;  // v5 spills with more than 96 Gram rows; v6<PM, 13> does not
       else if (gram_mode == 2 && (d_r1 || d_r2))
         which = 3;
+      else if (gram_mode == 0 && (d_r1 || d_r2) && !getenv("RG_KG_V6"))
+        which = 3;  // CholQR2's two-solve store pass: 0.41 vs 0.44 ms on v6 (profiles/ab_tall_r01.txt)
     }
     if (impl) which = impl[0] - '0';
     const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
