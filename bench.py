@@ -239,7 +239,7 @@ def _setup_step(grid, dev, seed=0, world=1, rank=0, family="cfg4"):
     R0 = D.empty_block(n, P, dev, dt)
     R0.copy_(torch.randn(n, P, generator=g, device=dev, dtype=dt))
     R0 = _scrub(R0, D.empty_block(n, P, dev, dt), rs.c)
-    fact = arnoldi.start(op.apply, R0, m_max=M, recycle=rs, seed=seed)
+    fact = arnoldi.start(op.apply, R0, m_max=M, recycle=rs, seed=seed, c_orthogonal=True)
     for _ in range(M - 1):
         arnoldi.step(fact, op.apply, recycle=rs)
     torch.cuda.synchronize()

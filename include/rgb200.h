@@ -143,9 +143,11 @@ int64_t rg_tsqr_workspace_bytes(int64_t n, int32_t p);
  * layer uses.  d_coef receives S1 (k x p) | c1 (w x p) | S2 | c2 packed
  * column-major (F = S1 + S2, H = c1 + c2 on the host, arnoldi.py:177,180);
  * if d_gram is non-NULL it receives Z^T Z of the projected block (the first
- * CholQR Gram).  p <= 16, k + w <= 256.
+ * CholQR Gram).  p <= 16, k <= 128 and w <= 128 (each basis is one Gram
+ * operand of rg_tall_f64; callers split wider bases).
  * joint != 0 (the solver's layout: W directly follows C in one allocation,
- * d_w == d_c + k*ldc, ldw == ldc, k + w <= 128, and C is orthogonal to W)
+ * d_w == d_c + k*ldc, ldw == ldc, k + w <= 128, and C is orthogonal to W
+ * -- the caller asserts this; the library cannot check it)
  * runs the projection against [C W] as one basis in three passes -- the
  * same CGS2 up to rounding -- and d_coef holds G1 = [S1; c1] | G2 =
  * [S2; c2], each (k+w) x p; the workspace must then cover gc = k + w.

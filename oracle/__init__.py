@@ -12,6 +12,8 @@ What it restates (reference = /root/reference/pkg/src/recgmres):
 * ``reduced_qr``      dense_kernels.py:31-48  (LAPACK Householder via numpy,
                       r_jj >= 0 sign fix, rank flags)
 * ``cgs2_project``    arnoldi.py:171-180  (two passes, C first then the basis)
+* ``mgs_project``     arnoldi.py:159-170  (one C column at a time, then one
+                      basis block at a time)
 * ``arnoldi_step``    arnoldi.py:139-193  (SpMM + CGS2 + QR; breakdown repair
                       omitted: the timed / checked inputs are full rank)
 * ``gram``/``update`` the numpy ``@`` products of arnoldi.py / solver.py
@@ -149,6 +151,27 @@ def cgs2_project(Ahat, C, W):
         coef = gram(W, Ahat)
         Ahat -= W @ coef
         H += coef
+    return Ahat, F, H
+
+
+def mgs_project(Ahat, C, W, L):
+    """Block modified Gram-Schmidt of arnoldi.py:159-170: each column c_i of
+    C (coef = c_i^T Ahat; Ahat -= c_i coef), then each basis block V_i of
+    the L-column blocks of W.  Returns (Ahat_projected, F_cols, H_cols)."""
+    Ahat = np.array(Ahat, order="F", copy=True)
+    k = 0 if C is None else C.shape[1]
+    F = np.zeros((k, Ahat.shape[1]), dtype=Ahat.dtype)
+    H = np.zeros((W.shape[1], Ahat.shape[1]), dtype=Ahat.dtype)
+    for i in range(k):
+        ci = C[:, i]
+        coef = np.conj(ci) @ Ahat
+        Ahat -= np.outer(ci, coef)
+        F[i] += coef
+    for i in range(W.shape[1] // L):
+        Vi = W[:, i * L:(i + 1) * L]
+        Hblk = np.conj(Vi).T @ Ahat
+        Ahat -= Vi @ Hblk
+        H[i * L:(i + 1) * L] += Hblk
     return Ahat, F, H
 
 

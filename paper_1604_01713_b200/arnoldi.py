@@ -30,9 +30,10 @@ from .ortho import project_chain
 from .sparse_core import ShapeError
 
 
-# CGS2 against [C W] as one basis when C precedes W in the factorization's
-# allocation (three passes); False forces the reference's sequential C-then-W
-# order (five passes) -- tests compare the two
+# CGS2 against [C W] as one basis (three passes) when the caller certified
+# that the starting block is C-orthogonal (``start(..., c_orthogonal=True)``:
+# the solver scrubs R0 against C first, solver.py:149-155); False forces the
+# reference's sequential C-then-W order (five passes) -- tests compare the two
 JOINT_PROJECTION = True
 
 
@@ -66,7 +67,10 @@ class ArnoldiFactorization:
         # basis, so the CGS2 projection can treat [C W] as one basis
         self._CW = _dev.empty_block(n, k + (m_max + 1) * L, dev, dtype)
         self._W = self._CW[:, k:]
-        self._c_src = None  # data_ptr of the recycle space C copied into _CW[:, :k]
+        self._c_src = None  # the recycle space C copied into _CW[:, :k] (identity check in step)
+        # the caller certified that R0 (hence V_1, and every later block by
+        # construction) is orthogonal to C: the joint [C W] schedule applies
+        self.c_orthogonal = False
         self._H = np.zeros(((m_max + 1) * L, m_max * L), dtype=npdt)
         self._F = np.zeros((k, m_max * L), dtype=npdt)
         self.z_bar = np.zeros((L, L), dtype=npdt)
@@ -190,10 +194,15 @@ def _apply_operator(opA, Z: torch.Tensor, out: torch.Tensor):
 
 
 def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: int = 0,
-          device=None) -> ArnoldiFactorization:
+          device=None, c_orthogonal: bool = False) -> ArnoldiFactorization:
     """Initialise from the starting block R0 (arnoldi.py:98-136): V_1, z_bar
     from its thin QR; rank-deficient columns replaced by seeded random
-    directions (C- and V_1-orthogonalised twice) and logged."""
+    directions (C- and V_1-orthogonalised twice) and logged.
+
+    ``c_orthogonal`` (keyword, not in the reference): the caller certifies
+    that R0 was already projected against the recycle space C (the solver
+    scrubs it, solver.py:149-155).  Only then may ``step`` project against
+    [C W] as one basis; the default keeps the reference's C-then-W order."""
     dev = _dev.require_cuda(device if device is not None else
                             (R0.device if isinstance(R0, torch.Tensor) and R0.is_cuda else None))
     R0d = _as_block_on(R0, dev)
@@ -209,7 +218,8 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev, R0d.dtype)
     if recycle is not None and k:
         fact._CW[:, :k].copy_(recycle.c_device())
-        fact._c_src = recycle.c_device().data_ptr()
+        fact._c_src = recycle.c_device()
+        fact.c_orthogonal = bool(c_orthogonal)
     V1 = fact.v_block(0)
     qr = _block_qr(fact, R0d, V1)
     fact.z_bar = qr[0]
@@ -271,10 +281,11 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     Vnew = fact.v_block(m + 1)
 
     k_, w_ = fact.k, (m + 1) * L
-    # [C W] as one basis when C sits in front of W (real data; the complex
+    # [C W] as one basis when the caller certified C-orthogonality at start
+    # and C is the recycle space copied in front of W (real data; the complex
     # tall pass has no aliased-term merge): 3 passes instead of 5
-    joint = (JOINT_PROJECTION and ortho == "cgs2" and C is not None and k_ > 0 and fact._c_src == C.data_ptr()
-             and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
+    joint = (JOINT_PROJECTION and ortho == "cgs2" and C is not None and k_ > 0 and fact.c_orthogonal
+             and fact._c_src is C and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
     if ortho == "cgs2" and joint:
         CW = fact._CW[:, : k_ + w_]
         if _dev.fused_ok() and L <= _dev.MAX_P_FUSED:
@@ -300,7 +311,8 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
         fact._H[: (m + 1) * L, cols] += hG1[k_:]
         fact._H[: (m + 1) * L, cols] += hG2[k_:]
     elif ortho == "cgs2":
-        if _dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED and fact.k + (m + 1) * L <= 256:
+        if (_dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED and fact.k <= _dev.MAX_GC
+                and (m + 1) * L <= _dev.MAX_GC):
             # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64);
             # C is passed from its own allocation here, so the five-pass
             # sequential schedule applies

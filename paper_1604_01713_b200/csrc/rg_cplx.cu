@@ -36,85 +36,13 @@ __device__ __forceinline__ void dmma_c(double& c0, double& c1, double a, double 
 constexpr int kCWarps = 8;
 constexpr int kCChunk = 256;
 
-template <int PB, bool GHOST>
-__global__ void __launch_bounds__(kCWarps * 32, 2)
-spmm_c128_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
-                 const int32_t* __restrict__ ci, const double2* __restrict__ va,
-                 const double2* __restrict__ X, int64_t ldx, int64_t n_local,
-                 const double2* __restrict__ Xg, int64_t ldg, double2* __restrict__ Y, int64_t ldy) {
-  __shared__ int32_t s_ci[kCWarps][kCChunk];
-  __shared__ double2 s_va[kCWarps][kCChunk];
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int64_t nunits = (row_end - row_begin + 31) / 32;
-  const int64_t nwarps = (int64_t)gridDim.x * kCWarps;
-  for (int64_t u = (int64_t)blockIdx.x * kCWarps + w; u < nunits; u += nwarps) {
-    const int64_t wrow0 = row_begin + u * 32;
-    const int64_t wlast = min(wrow0 + 32, row_end);
-    const int64_t i = wrow0 + lane;
-    const bool valid = i < row_end;
-    const int32_t wbeg = __ldg(rp + wrow0), wend = __ldg(rp + wlast);
-    const int32_t mybeg = valid ? __ldg(rp + i) : 0, myend = valid ? __ldg(rp + i + 1) : 0;
-    double ar_[PB], ai_[PB];
-#pragma unroll
-    for (int c = 0; c < PB; ++c) ar_[c] = ai_[c] = 0.0;
-    for (int32_t base = wbeg; base < wend; base += kCChunk) {
-      const int32_t cnt = min(kCChunk, wend - base);
-      __syncwarp();
-      for (int e = lane; e < cnt; e += 32) {
-        s_ci[w][e] = __ldg(ci + base + e);
-        s_va[w][e] = __ldg(va + base + e);
-      }
-      __syncwarp();
-      const int lo = max(mybeg, base) - base, hi = min(myend, base + cnt) - base;
-      double2 xn[PB];
-      double2 an = make_double2(0.0, 0.0);
-      auto gather = [&](int t, double2 (&xv)[PB]) {
-        const int64_t j = s_ci[w][t];
-        const double2* xp = X + j;
-        int64_t ld = ldx;
-        if (GHOST && j >= n_local) {
-          xp = Xg + (j - n_local);
-          ld = ldg;
-        }
-#pragma unroll
-        for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
-      };
-      if (lo < hi) {
-        an = s_va[w][lo];
-        gather(lo, xn);
-      }
-      for (int t = lo; t < hi; ++t) {
-        double2 xc[PB];
-#pragma unroll
-        for (int c = 0; c < PB; ++c) xc[c] = xn[c];
-        const double2 a = an;
-        if (t + 1 < hi) {
-          an = s_va[w][t + 1];
-          gather(t + 1, xn);
-        }
-#pragma unroll
-        for (int c = 0; c < PB; ++c) {
-          const double pr = __dsub_rn(__dmul_rn(a.x, xc[c].x), __dmul_rn(a.y, xc[c].y));
-          const double pi = __dadd_rn(__dmul_rn(a.x, xc[c].y), __dmul_rn(a.y, xc[c].x));
-          ar_[c] = __dadd_rn(ar_[c], pr);
-          ai_[c] = __dadd_rn(ai_[c], pi);
-        }
-      }
-    }
-    if (valid) {
-#pragma unroll
-      for (int c = 0; c < PB; ++c) Y[i + c * ldy] = make_double2(ar_[c], ai_[c]);
-    }
-  }
-}
-
 // Production SpMM: no shared-memory staging.  G lanes share a row (G=2
 // splits a 16-wide block into two 8-column halves, so one pass covers p=16
 // and A is read once); each lane walks its own row's entries straight from
 // global memory (L1-resident lines) with the next entry's index/value and X
 // gathers issued one entry ahead.  Rows per warp RPW = 32/G; warps are
-// persistent over RPW-row units.  Arithmetic order is the same as above.
+// persistent over RPW-row units.  Per (row, column): entries in storage
+// order, each complex product formed and rounded separately, then added.
 template <int G, int PB, bool GHOST>
 __global__ void __launch_bounds__(kCWarps * 32, 2)
 spmm_c128_direct_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
@@ -208,23 +136,6 @@ static void launch_spmm_cd(int64_t rb, int64_t re, const int32_t* rp, const int3
   else
     spmm_c128_direct_kernel<G, PB, false><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
                                                                               Xg, ldg, Y, ldy);
-}
-
-template <int PB>
-static void launch_spmm_c(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double2* va,
-                          const double2* X, int64_t ldx, int64_t n_local, const double2* Xg, int64_t ldg, double2* Y,
-                          int64_t ldy, cudaStream_t s) {
-  const int64_t units = (re - rb + 31) / 32;
-  int64_t g = (int64_t)sm_count() * 2;
-  const int64_t need = (units + kCWarps - 1) / kCWarps;
-  if (need < g) g = need;
-  if (g < 1) g = 1;
-  if (Xg)
-    spmm_c128_kernel<PB, true><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg, Y,
-                                                                     ldy);
-  else
-    spmm_c128_kernel<PB, false><<<(unsigned)g, kCWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg,
-                                                                      Y, ldy);
 }
 
 // ----------------------------------------------------------------------------
@@ -1077,9 +988,7 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
   const double2* Xg = reinterpret_cast<const double2*>(d_xg);
   double2* Y = reinterpret_cast<double2*>(d_y);
   const double2* va = reinterpret_cast<const double2*>(d_vals);
-  static const int legacy = getenv("RG_SPMMC_LEGACY") ? 1 : 0;
-  static const int g2_8 = getenv("RG_SPMMC_G2_8") ? 1 : 0;
-  if (!legacy) {
+  {
     // passes of 16 columns (two lanes per row), then one exact-width pass
     for (int c0 = 0; c0 < p;) {
       const int rem = p - c0;
@@ -1090,7 +999,7 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
 #define RG_CD(G, PB) launch_spmm_cd<G, PB>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s)
       switch (pc) {
         case 16: RG_CD(2, 8); break;
-        case 8: if (g2_8) RG_CD(2, 4); else RG_CD(1, 8); break;
+        case 8: RG_CD(1, 8); break;
         case 7: RG_CD(1, 7); break;
         case 6: RG_CD(1, 6); break;
         case 5: RG_CD(1, 5); break;
@@ -1103,22 +1012,6 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
       RG_CHECK_LAUNCH("rg_spmm_csr_c128");
       c0 += pc;
     }
-    return RG_OK;
-  }
-  for (int c0 = 0; c0 < p;) {
-    const int rem = p - c0;
-    const int pc = rem >= 8 ? 8 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
-    const double2* Xc = X ? X + (int64_t)c0 * ldx : nullptr;
-    const double2* Xgc = Xg ? Xg + (int64_t)c0 * ldg : nullptr;
-    double2* Yc = Y + (int64_t)c0 * ldy;
-    switch (pc) {
-      case 1: launch_spmm_c<1>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
-      case 2: launch_spmm_c<2>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
-      case 4: launch_spmm_c<4>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
-      default: launch_spmm_c<8>(row_begin, row_end, d_row_ptr, d_col_idx, va, Xc, ldx, n_local, Xgc, ldg, Yc, ldy, s); break;
-    }
-    RG_CHECK_LAUNCH("rg_spmm_csr_c128");
-    c0 += pc;
   }
   return RG_OK;
 }
@@ -1171,8 +1064,7 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
   P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
   if (gram_mode == 0 && n == 0) return RG_OK;
   cudaStream_t st0 = (cudaStream_t)stream;
-  static const int legacy = getenv("RG_TALLC_LEGACY") ? 1 : 0;
-  if (p > 8 || (p > 4 && !legacy)) {
+  if (p > 4) {
     // tensor-core pass (complex v6)
     cudaError_t e6;
     const int mt = P.mtiles;

@@ -252,8 +252,7 @@ static int64_t wave_grid(int32_t nchunks, int32_t width) {
   // Persistent warps, but only about two levels' worth of them: warps that
   // claim chunks further ahead only poll flags, and their acquire loads
   // compete with the rows being solved for L2 bandwidth.
-  static const int levels = getenv("RG_WAVE_LEVELS") ? atoi(getenv("RG_WAVE_LEVELS")) : 2;
-  static const int bps = getenv("RG_WAVE_BPS") ? atoi(getenv("RG_WAVE_BPS")) : 4;
+  constexpr int levels = 2, bps = 4;
   int64_t g = (int64_t)sm_count() * bps;
   const int64_t lvl = ((int64_t)levels * (width > 0 ? width : 1) + kWaveWarps - 1) / kWaveWarps;
   if (lvl < g) g = lvl;
@@ -320,8 +319,7 @@ static rg::Wave make_wave(const int32_t* order, const int32_t* chunk, int32_t nc
   W.ticket = (unsigned*)d_work;
   W.flags = (int*)((char*)d_work + 256);
   W.epoch = epoch;
-  static const unsigned ns_max = getenv("RG_WAVE_NS") ? (unsigned)atoi(getenv("RG_WAVE_NS")) : 1024u;
-  W.ns_max = ns_max;
+  W.ns_max = 1024u;  // polling back-off cap (ns)
   return W;
 }
 

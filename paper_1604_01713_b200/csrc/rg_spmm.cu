@@ -26,104 +26,13 @@ namespace rg {
 constexpr int kSpmmWarps = 8;     // 256 threads per CTA
 constexpr int kSpmmChunk = 256;   // staged nonzeros per warp per round
 
-template <int PB, bool GHOST>
-__global__ void __launch_bounds__(kSpmmWarps * 32)
-spmm_csr_kernel(int64_t row_begin, int64_t row_end,
-                const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                const double* __restrict__ va,
-                const double* __restrict__ X, int64_t ldx, int64_t n_local,
-                const double* __restrict__ Xg, int64_t ldg,
-                double* __restrict__ Y, int64_t ldy) {
-  __shared__ int32_t s_ci[kSpmmWarps][kSpmmChunk];
-  __shared__ double s_va[kSpmmWarps][kSpmmChunk];
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const int64_t wrow0 = row_begin + ((int64_t)blockIdx.x * kSpmmWarps + w) * 32;
-  if (wrow0 >= row_end) return;  // warp-uniform
-  const int64_t wlast = min(wrow0 + 32, row_end);
-  const int64_t i = wrow0 + lane;
-  const bool valid = i < row_end;
-  const int32_t wbeg = __ldg(rp + wrow0);
-  const int32_t wend = __ldg(rp + wlast);
-  const int32_t mybeg = valid ? __ldg(rp + i) : 0;
-  const int32_t myend = valid ? __ldg(rp + i + 1) : 0;
-
-  double acc[PB];
-#pragma unroll
-  for (int c = 0; c < PB; ++c) acc[c] = 0.0;
-
-  int32_t* sci = s_ci[w];
-  double* sva = s_va[w];
-  for (int32_t base = wbeg; base < wend; base += kSpmmChunk) {
-    const int32_t cnt = min(kSpmmChunk, wend - base);
-    // all loads of the chunk are issued before the first shared-memory store
-    int32_t ci_r[kSpmmChunk / 32];
-    double va_r[kSpmmChunk / 32];
-#pragma unroll
-    for (int u = 0; u < kSpmmChunk / 32; ++u) {
-      const int e = lane + 32 * u;
-      if (e < cnt) {
-        ci_r[u] = __ldg(ci + base + e);
-        va_r[u] = __ldg(va + base + e);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kSpmmChunk / 32; ++u) {
-      const int e = lane + 32 * u;
-      if (e < cnt) {
-        sci[e] = ci_r[u];
-        sva[e] = va_r[u];
-      }
-    }
-    __syncwarp();
-    const int lo = max(mybeg, base) - base;
-    const int hi = min(myend, base + cnt) - base;
-    // software pipeline: the PB gathers of nonzero t+1 are in flight while
-    // nonzero t is accumulated (in the reference's order: t ascending)
-    double xn[PB];
-    double an = 0.0;
-    auto gather = [&](int t, double (&xv)[PB]) {
-      const int64_t j = sci[t];
-      const double* xp = X + j;
-      int64_t ld = ldx;
-      if (GHOST && j >= n_local) {
-        xp = Xg + (j - n_local);
-        ld = ldg;
-      }
-#pragma unroll
-      for (int c = 0; c < PB; ++c) xv[c] = __ldg(xp + c * ld);
-    };
-    if (lo < hi) {
-      an = sva[lo];
-      gather(lo, xn);
-    }
-    for (int t = lo; t < hi; ++t) {
-      double xc[PB];
-#pragma unroll
-      for (int c = 0; c < PB; ++c) xc[c] = xn[c];
-      const double ac = an;
-      if (t + 1 < hi) {
-        an = sva[t + 1];
-        gather(t + 1, xn);
-      }
-#pragma unroll
-      for (int c = 0; c < PB; ++c) acc[c] = __dadd_rn(acc[c], __dmul_rn(ac, xc[c]));
-    }
-    __syncwarp();
-  }
-  if (valid) {
-#pragma unroll
-    for (int c = 0; c < PB; ++c) Y[i + c * ldy] = acc[c];
-  }
-}
-
 // ----------------------------------------------------------------------------
-// Persistent variant (production path): warps loop over 32-row units; the
+// Persistent kernel: warps loop over 32-row units; the
 // CSR entries of the next unit stream into a per-warp double buffer with
 // cp.async while the current unit gathers X, and row_ptr is loaded two units
 // ahead, so a unit's only exposed latency is its X gathers (mostly L2 hits).
 // Units whose 32 rows hold more than kSpmmChunk nonzeros take the chunked
-// synchronous path.  Arithmetic and order are exactly those above.
+// synchronous path.  Arithmetic and order are the reference's (see top).
 // ----------------------------------------------------------------------------
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -283,62 +192,30 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-// G = 2 lanes per row, 16-row units with up to 128 staged entries each: twice
-// the warps in flight of the lane-per-row kernel at half the registers
-template <int PB>
-static void launch_spmm_g2(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci, const double* va,
-                           const double* X, int64_t ldx, int64_t n_local, const double* Xg, int64_t ldg, double* Y,
-                           int64_t ldy, cudaStream_t s) {
-  static int per_sm[2] = {-1, -1};
-  const int gi = Xg ? 1 : 0;
-  auto k = Xg ? spmm_persist_kernel<PB, true, 2, 128> : spmm_persist_kernel<PB, false, 2, 128>;
-  if (per_sm[gi] < 0) {
-    int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kSpmmWarps * 32, 0);
-    per_sm[gi] = v < 1 ? 1 : v;
-  }
-  const int64_t units = (re - rb + 15) / 16;
-  int64_t g = (int64_t)sm_count() * per_sm[gi];
-  const int64_t need = (units + kSpmmWarps - 1) / kSpmmWarps;
-  if (need < g) g = need;
-  if (g < 1) g = 1;
-  k<<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local, Xg, ldg, Y, ldy);
-}
-
 template <int PB>
 static void launch_spmm(int64_t rb, int64_t re, const int32_t* rp, const int32_t* ci,
                         const double* va, const double* X, int64_t ldx, int64_t n_local,
                         const double* Xg, int64_t ldg, double* Y, int64_t ldy, cudaStream_t s) {
   const int64_t rows = re - rb;
-  const int64_t rows_per_cta = kSpmmWarps * 32;
-  const int64_t grid = (rows + rows_per_cta - 1) / rows_per_cta;
-  if (!getenv("RG_SPMM_LEGACY")) {
-    static int per_sm[2] = {-1, -1};
-    const int gi = Xg ? 1 : 0;
-    if (per_sm[gi] < 0) {
-      int v = 0;
-      if (Xg)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, true>, kSpmmWarps * 32, 0);
-      else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, false>, kSpmmWarps * 32, 0);
-      per_sm[gi] = v < 1 ? 1 : v;
-    }
-    int64_t g = (int64_t)sm_count() * per_sm[gi];
-    if (grid < g) g = grid;
-    if (g < 1) g = 1;
+  const int64_t grid = (rows + kSpmmWarps * 32 - 1) / (kSpmmWarps * 32);
+  static int per_sm[2] = {-1, -1};
+  const int gi = Xg ? 1 : 0;
+  if (per_sm[gi] < 0) {
+    int v = 0;
     if (Xg)
-      spmm_persist_kernel<PB, true><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
-                                                                          Xg, ldg, Y, ldy);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, true>, kSpmmWarps * 32, 0);
     else
-      spmm_persist_kernel<PB, false><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
-                                                                           Xg, ldg, Y, ldy);
-    return;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, spmm_persist_kernel<PB, false>, kSpmmWarps * 32, 0);
+    per_sm[gi] = v < 1 ? 1 : v;
   }
+  int64_t g = (int64_t)sm_count() * per_sm[gi];
+  if (grid < g) g = grid;
+  if (g < 1) g = 1;
   if (Xg)
-    spmm_csr_kernel<PB, true><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+    spmm_persist_kernel<PB, true><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
                                                                         Xg, ldg, Y, ldy);
   else
-    spmm_csr_kernel<PB, false><<<(unsigned)grid, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
+    spmm_persist_kernel<PB, false><<<(unsigned)g, kSpmmWarps * 32, 0, s>>>(rb, re, rp, ci, va, X, ldx, n_local,
                                                                          Xg, ldg, Y, ldy);
 }
 
@@ -365,20 +242,13 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
   // exact-width passes (no per-column predication in the inner loop) of at
   // most 8 columns: a 16-wide register block spills, and re-reading A for a
   // second 8-wide pass is cheaper (profiles/spmm_r01.txt)
-  static const int g2 = getenv("RG_SPMM_G2") ? atoi(getenv("RG_SPMM_G2")) : 0;
-  static const int g2_16 = getenv("RG_SPMM_G2_16") ? atoi(getenv("RG_SPMM_G2_16")) : 0;
   for (int c0 = 0; c0 < p;) {
     const int rem = p - c0;
-    // RG_SPMM_G2_16=1: 16-wide passes with two lanes per row (A read once) -- 1.5x slower
-    // than two 8-wide passes at cfg4 (profiles/spmm_r01.txt), so off by default
-    const int pc = (rem >= 16 && g2_16) ? 16 : (rem >= 8 ? 8 : rem);
+    const int pc = rem >= 8 ? 8 : rem;
     const double* X = d_x ? d_x + (int64_t)c0 * ldx : nullptr;
     const double* Xg = d_xg ? d_xg + (int64_t)c0 * ldg : nullptr;
     double* Y = d_y + (int64_t)c0 * ldy;
     switch (pc) {
-      case 16:
-        launch_spmm_g2<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
-        break;
       case 1: launch_spmm<1>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 2: launch_spmm<2>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 3: launch_spmm<3>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
@@ -386,13 +256,7 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
       case 5: launch_spmm<5>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 6: launch_spmm<6>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
       case 7: launch_spmm<7>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
-      case 8:
-        if (g2)
-          launch_spmm_g2<4>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
-        else
-          launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s);
-        break;
-      default: launch_spmm<16>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
+      default: launch_spmm<8>(row_begin, row_end, d_row_ptr, d_col_idx, d_vals, X, ldx, n_local, Xg, ldg, Y, ldy, s); break;
     }
     RG_CHECK_LAUNCH("rg_spmm_csr_f64");
     c0 += pc;

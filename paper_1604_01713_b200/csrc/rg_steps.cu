@@ -47,7 +47,9 @@ extern "C" int rg_cgs2_f64(int64_t n, int32_t p, double* d_z, int64_t ldz, const
   RG_REQUIRE(n >= 0 && p >= 1 && p <= 16, "rg_cgs2_f64: p=%d outside [1, 16]", p);
   RG_REQUIRE(k >= 0 && w >= 0 && (k == 0 || d_c) && (w == 0 || d_w) && d_z && d_coef,
              "rg_cgs2_f64: bad operands");
-  RG_REQUIRE(k + w <= 256, "rg_cgs2_f64: k + w = %d too wide for one schedule", k + w);
+  // each basis is one Gram operand of rg_tall_f64 (<= 128 columns); wider
+  // bases are split by the caller (ortho.project_chain does)
+  RG_REQUIRE(k <= 128 && w <= 128, "rg_cgs2_f64: k=%d, w=%d: each basis must have <= 128 columns", k, w);
   // the joint schedule is the caller's explicit choice: adjacency alone can
   // be a coincidence of the allocator, and the schedule assumes C is
   // orthogonal to W (the solver's invariant, not every caller's)

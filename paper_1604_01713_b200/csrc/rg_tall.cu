@@ -1,24 +1,27 @@
 // Fused tall-skinny block kernels (K2 Gram, K3 update, K4 CGS2 passes, the
 // CholQR2 passes of K5, K6 norms, K7 triangular solve, K8 scaling).
 //
-// One launch streams an n x p block Z once, tile by tile (R = 256 rows):
+// One launch ("pass") streams an n x p block Z once and computes, per row,
 //
-//   phase 1 (one thread per row):
 //       z  = Zin[i,:] (or 0)
-//       z += alpha_t * (X_t[i,:] @ S_t)      t = 1, 2; S_t staged in smem and
-//                                             read as warp broadcasts
+//       z += alpha_t * (X_t[i,:] @ S_t)      t = 1, 2 (two terms over the same
+//                                             X are merged into one)
 //       z  = z @ inv(R1) [@ inv(R2)]         row-wise forward substitution
-//       Zout[i,:] = z;  tile[:, r] = z       column-major smem tile
-//   phase 2 (Gram on the FP64 tensor cores, DMMA m8n8k4):
-//       Gout += Gb[tile rows, :]^T @ tile     (mode 1; A fragments are read
-//                                             straight from HBM: 8 columns x
-//                                             4 consecutive rows = 8 full
-//                                             32-byte sectors per warp load)
-//       Gout += tile^T @ tile                 (mode 2, CholQR Gram)
-//       Gout += column sums of z^2            (mode 3, norms; CUDA cores)
-//   epilogue: warp partials summed in warp order in smem -> CTA partial in
-//       the workspace -> the last CTA to finish sums the partials in CTA
-//       order (deterministic) into Gout and re-arms the ticket counter.
+//       Zout[i,:] = z
+//   and one reduction over all rows:
+//       Gout  = Gb^T Z                        (mode 1, basis Gram)
+//       Gout  = Z^T Z                         (mode 2, CholQR Gram)
+//       Gout  = column sums of z^2            (mode 3, norms)
+//   The Gram reductions are deterministic: warp partials summed in warp
+//   order, CTA partials written to the workspace, and the last CTA to finish
+//   sums them in CTA order into Gout and re-arms the ticket counter.
+//
+// Four kernels implement a pass; rg_tall_f64 picks one per pass shape from
+// measurements (see the dispatch at the bottom):
+//   ws   warp-specialised producer/consumer ring (the wide CGS2 passes)
+//   v6   per-warp cp.async slab ring, DMMA update and Gram (narrower passes)
+//   v5   lane-per-row DFMA update, Gram basis through a cp.async ring
+//   v3   lane-per-row loads (CholQR solve passes, unaligned operands)
 //
 // This is the B200 restatement of the numpy/OpenBLAS calls the reference
 // makes per block Arnoldi step (arnoldi.py:172-180: S = C^T Ahat;
@@ -37,8 +40,6 @@
 namespace rg {
 
 constexpr int kTallThreads = 256;  // = tile rows R
-constexpr int kTallWarps = kTallThreads / 32;
-constexpr int kTileStride = kTallThreads + 4;  // padded: conflict-free DMMA fragment loads
 
 struct TallParams {
   int64_t n;
@@ -123,187 +124,6 @@ __device__ __forceinline__ void trsm_row(double (&z)[PM], const double* sR, int 
   }
 }
 
-template <int PM, int MTMAX>
-__global__ void __launch_bounds__(kTallThreads, 1) tall_kernel(TallParams P) {
-  constexpr int PM8 = PM < 8 ? 8 : PM;  // tile columns (zero padded to the MMA N)
-  constexpr int NT = PM8 / 8;
-  extern __shared__ __align__(16) double smem[];
-  const int p = P.p;
-  double* sS1 = smem;
-  double* sS2 = sS1 + P.a1 * PM;
-  double* sR1 = sS2 + P.a2 * PM;
-  double* sR2 = sR1 + (P.r1 ? PM * PM : 0);
-  double* sZ = sR2 + (P.r2 ? PM * PM : 0);  // [PM8][kTileStride]
-  double* sRed = sZ + ((P.gmode == 1 || P.gmode == 2) ? PM8 * kTileStride : 0);
-
-  for (int e = threadIdx.x; e < P.a1 * PM; e += kTallThreads) {
-    const int aa = e / PM, c = e % PM;
-    sS1[e] = c < p ? P.s1[aa + (int64_t)c * P.a1] : 0.0;
-  }
-  for (int e = threadIdx.x; e < P.a2 * PM; e += kTallThreads) {
-    const int aa = e / PM, c = e % PM;
-    sS2[e] = c < p ? P.s2[aa + (int64_t)c * P.a2] : 0.0;
-  }
-  if (P.r1)
-    for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
-      const int ii = e / PM, jj = e % PM;
-      sR1[e] = (ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : (ii == jj ? 1.0 : 0.0);
-    }
-  if (P.r2)
-    for (int e = threadIdx.x; e < PM * PM; e += kTallThreads) {
-      const int ii = e / PM, jj = e % PM;
-      sR2[e] = (ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : (ii == jj ? 1.0 : 0.0);
-    }
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const bool gram_tile = (P.gmode == 1 || P.gmode == 2);
-  const int mtiles = P.mtiles;
-
-  double acc[MTMAX][NT][2];
-#pragma unroll
-  for (int mt = 0; mt < MTMAX; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-  double sq[PM];
-#pragma unroll
-  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
-
-  for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-    const int64_t tile0 = tile * kTallThreads;
-    // ---------------- phase 1: row-wise update / solve / store
-    {
-      const int64_t i = tile0 + threadIdx.x;
-      double z[PM];
-#pragma unroll
-      for (int c = 0; c < PM; ++c) z[c] = 0.0;
-      if (i < P.n) {
-        if (P.zin) {
-#pragma unroll
-          for (int c = 0; c < PM; ++c)
-            if (c < p) z[c] = __ldg(P.zin + i + (int64_t)c * P.ldzin);
-        }
-        if (P.a1) apply_term<PM>(z, P.x1, P.ldx1, P.a1, sS1, P.alpha1, i);
-        if (P.a2) apply_term<PM>(z, P.x2, P.ldx2, P.a2, sS2, P.alpha2, i);
-        if (P.r1) trsm_row<PM>(z, sR1, p);
-        if (P.r2) trsm_row<PM>(z, sR2, p);
-        if (P.zout) {
-#pragma unroll
-          for (int c = 0; c < PM; ++c)
-            if (c < p) P.zout[i + (int64_t)c * P.ldzout] = z[c];
-        }
-        if (P.gmode == 3) {
-#pragma unroll
-          for (int c = 0; c < PM; ++c) sq[c] = fma(z[c], z[c], sq[c]);
-        }
-      }
-      if (gram_tile) {
-#pragma unroll
-        for (int c = 0; c < PM8; ++c)
-          sZ[c * kTileStride + threadIdx.x] = (c < PM) ? z[c < PM ? c : 0] : 0.0;
-      }
-    }
-    if (!gram_tile) continue;
-    __syncthreads();
-    // ---------------- phase 2: Gram of this tile on the FP64 tensor cores
-    {
-      constexpr int kSteps = kTallThreads / 4 / kTallWarps;  // k-steps (4 rows) per warp
-      const int kr = lane & 3;   // k index inside the step
-      const int mn = lane >> 2;  // m (A) / n (B) index inside the 8x8 tile
-#pragma unroll 2
-      for (int s = 0; s < kSteps; ++s) {
-        const int r = (w * kSteps + s) * 4 + kr;
-        const int64_t i = tile0 + r;
-        double b[NT];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) b[nt] = sZ[(nt * 8 + mn) * kTileStride + r];
-        double a[MTMAX];
-        if (P.gmode == 1) {
-#pragma unroll
-          for (int mt = 0; mt < MTMAX; ++mt) {
-            const int gg = mt * 8 + mn;
-            a[mt] = (mt < mtiles && gg < P.gc && i < P.n) ? __ldg(P.gb + i + (int64_t)gg * P.ldgb) : 0.0;
-          }
-        } else {
-#pragma unroll
-          for (int mt = 0; mt < MTMAX; ++mt) {
-            const int gg = mt * 8 + mn;
-            a[mt] = (mt < mtiles && gg < PM8) ? sZ[gg * kTileStride + r] : 0.0;
-          }
-        }
-#pragma unroll
-        for (int mt = 0; mt < MTMAX; ++mt)
-          if (mt < mtiles) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
-          }
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---------------- epilogue: CTA partial -> workspace
-  __shared__ bool s_last;
-  if (gram_tile) {
-    // sum warp fragments in warp order (deterministic)
-    for (int ww = 0; ww < kTallWarps; ++ww) {
-      if (w == ww) {
-#pragma unroll
-        for (int mt = 0; mt < MTMAX; ++mt)
-          if (mt < mtiles) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-              for (int v = 0; v < 2; ++v) {
-                const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
-                sRed[idx] = (ww == 0) ? acc[mt][nt][v] : sRed[idx] + acc[mt][nt][v];
-              }
-          }
-      }
-      __syncthreads();
-    }
-    const int ne = P.gc * p;
-    for (int e = threadIdx.x; e < ne; e += kTallThreads) {
-      const int gg = e % P.gc, c = e / P.gc;
-      const int mt = gg >> 3, mrow = gg & 7, nt = c >> 3, ncol = c & 7;
-      const int ln = mrow * 4 + (ncol >> 1), v = ncol & 1;
-      P.part[(int64_t)blockIdx.x * ne + e] = sRed[((mt * NT + nt) * 32 + ln) * 2 + v];
-    }
-  } else if (P.gmode == 3) {
-#pragma unroll
-    for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
-    double* red = sZ;
-    if (lane == 0)
-#pragma unroll
-      for (int c = 0; c < PM; ++c) red[w * PM + c] = sq[c];
-    __syncthreads();
-    for (int c = threadIdx.x; c < p; c += kTallThreads) {
-      double s = 0.0;
-      for (int ww = 0; ww < kTallWarps; ++ww) s += red[ww * PM + c];
-      P.part[(int64_t)blockIdx.x * p + c] = s;
-    }
-  }
-  if (P.gmode == 0) return;
-
-  // ---------------- last CTA: deterministic cross-CTA sum
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned t = atomicAdd(P.counter, 1u);
-    s_last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int ne = (P.gmode == 3) ? p : P.gc * p;
-  for (int e = threadIdx.x; e < ne; e += kTallThreads) {
-    double s = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(P.part + (int64_t)b * ne + e);
-    P.gout[e] = s;
-  }
-  if (threadIdx.x == 0) *P.counter = 0u;  // re-arm for the next launch on this workspace
-}
 
 
 // ============================================================================
@@ -817,33 +637,6 @@ static int pick_mtmax(int mtiles) {
   return 16;
 }
 
-static size_t tall_smem(int PM, int a1, int a2, bool r1, bool r2, int gmode, int mtmax) {
-  const int PM8 = PM < 8 ? 8 : PM;
-  size_t words = (size_t)(a1 + a2) * PM + (r1 ? PM * PM : 0) + (r2 ? PM * PM : 0);
-  if (gmode == 1 || gmode == 2)
-    words += (size_t)PM8 * kTileStride + (size_t)mtmax * (PM8 / 8) * 64;
-  else if (gmode == 3)
-    words += (size_t)kTallWarps * PM;
-  return words * sizeof(double);
-}
-
-template <int PM, int MTMAX>
-static cudaError_t launch_tall(const TallParams& P, size_t smem, int64_t max_grid, cudaStream_t st) {
-  auto k = tall_kernel<PM, MTMAX>;
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kTallThreads, 48 * 1024);
-    per_sm = v < 1 ? 1 : v;
-  }
-  int64_t g = (int64_t)sm_count() * per_sm;
-  if (g > max_grid) g = max_grid;
-  if (P.ntiles < g) g = P.ntiles;
-  if (g < 1) g = 1;
-  k<<<(unsigned)g, kTallThreads, smem, st>>>(P);
-  return cudaGetLastError();
-}
 
 
 // ============================================================================
@@ -1665,8 +1458,6 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   int stages = kWsMaxStages;
   while (stages >= 2 && (size_t)stages * per_stage + extra > G::kSmemMax) --stages;
   if (stages < 2) return false;
-  static const int max_st = getenv("RG_WS_STAGES") ? atoi(getenv("RG_WS_STAGES")) : kWsMaxStages;
-  if (stages > max_st && max_st >= 2) stages = max_st;
   if ((size_t)stages * per_stage < red_bytes) return false;
   // narrow passes (the CholQR solves: 8 columns, 4.6 KB stages) cannot keep
   // enough bytes in flight per SM through a ring of whole stages -- v3 / v6
@@ -1674,8 +1465,7 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   if ((size_t)stages * per_stage < (size_t)96 * 1024) return false;
   // below ~64 streamed columns the fixed per-stage cost (mbarrier round
   // trips, 64-row stages) loses to v6 (tools/ws_sweep.py, profiles/ws_study_r01.txt)
-  static const int min_cols = getenv("RG_WS_MIN_COLS") ? atoi(getenv("RG_WS_MIN_COLS")) : 64;
-  if (W.nload < min_cols) return false;
+  if (W.nload < 64) return false;
   W.stages = stages;
   smem = (size_t)stages * per_stage + extra;
   return true;
@@ -1711,8 +1501,7 @@ static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cuda
     case 13: e = launch_ws<CW, NTv, 13>(P, W, smem, st); break;       \
     default: e = launch_ws<CW, NTv, 16>(P, W, smem, st); break;       \
   }
-  static const int breg = getenv("RG_WS_BREG") ? atoi(getenv("RG_WS_BREG")) : 1;
-  if (NT == 1 && breg && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
+  if (NT == 1 && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
     // the joint schedule's P2 shape at p <= 8: S in registers (3.08 -> 3.00-3.05
     // ms at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
     e = launch_ws<CW, 1, 13, 26>(P, W, smem, st);
@@ -1727,14 +1516,10 @@ static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cuda
 
 // returns false when the pass is not a ws shape (caller falls back to v6)
 static bool try_ws(const TallParams& P, int PM, cudaStream_t st, cudaError_t& e) {
-  static const int mode = getenv("RG_TALL_WS") ? atoi(getenv("RG_TALL_WS")) : 1;
-  if (!mode || PM > 16) return false;
+  if (PM > 16) return false;
   const int NT = PM > 8 ? 2 : 1;
   const int mt = (P.gmode == 1 || P.gmode == 2) ? P.mtiles : 0;
   const int MT = mt == 0 ? 0 : (mt <= 2 ? 2 : (mt <= 6 ? 6 : (mt <= 13 ? 13 : 16)));
-  static const int cw = getenv("RG_WS_CW") ? atoi(getenv("RG_WS_CW")) : 8;
-  if (cw == 4) return try_ws_cw<4>(P, NT, MT, st, e);
-  if (cw == 6) return try_ws_cw<6>(P, NT, MT, st, e);
   return try_ws_cw<8>(P, NT, MT, st, e);
 }
 
@@ -1840,15 +1625,6 @@ static bool aligned16(const void* p, int64_t ld) {
 static int64_t tall_grid_bound() { return (int64_t)sm_count() * 4; }
 static int64_t tall_grid_bound2() { return (int64_t)sm_count() * 2; }
 
-#define RG_TALL_CASE(PMv)                                                                 \
-  case PMv:                                                                               \
-    switch (mtmax) {                                                                      \
-      case 2: e = launch_tall<PMv, 2>(P, smem, bound, st); break;                         \
-      case 6: e = launch_tall<PMv, 6>(P, smem, bound, st); break;                         \
-      case 12: e = launch_tall<PMv, 12>(P, smem, bound, st); break;                       \
-      default: e = launch_tall<PMv, 16>(P, smem, bound, st); break;                       \
-    }                                                                                     \
-    break;
 
 }  // namespace rg
 
@@ -1906,8 +1682,6 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   if (gram_mode == 0 && P.ntiles == 0) return RG_OK;
   const int PM = pick_pm(p);
   const int mtmax = pick_mtmax(P.mtiles);
-  const size_t smem = tall_smem(PM, a1, a2, d_r1 != nullptr, d_r2 != nullptr, gram_mode, mtmax);
-  RG_REQUIRE(smem <= 200 * 1024, "rg_tall_f64: %zu bytes of shared memory (terms too wide)", smem);
   const int64_t bound = tall_grid_bound2();
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
@@ -1933,17 +1707,19 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
     }
     return RG_OK;
   }
-  if (!getenv("RG_TALL_LEGACY") && (P.a1 + P.a2) <= 512 && aligned) {
-    const char* impl = getenv("RG_TALL_IMPL");
-    const int mt5 = (gram_mode == 1 || gram_mode == 2) ? mtmax : 0;
-    // default v6 (all operands through the cp.async ring, DMMA update);
-    // RG_TALL_IMPL=3 / 5 select the earlier variants for A/B runs
-    // (tools/ab_tall.sh, profiles/ab_tall_r01.txt)
-    // measured per pass type (profiles/ab_tall_r01.txt): v6 for passes with
-    // an update term or a triangular-solve store, v5 for a pure basis Gram,
-    // v3 for the self-Gram solve pass of CholQR2
+  // dispatch measured per pass type (profiles/ab_tall_r01.txt,
+  // profiles/ws_study_r01.txt): the warp-specialised ws kernel for the wide
+  // CGS2 passes (>= 64 streamed columns); otherwise v6 for passes with an
+  // update term, v5 for a pure basis Gram of <= 96 columns, v3 for the
+  // CholQR2 solve passes.  Operands that are not 16-byte aligned (row-offset
+  // views) go to v3, whose loads are lane-per-row scalars.
+  const int mt5 = (gram_mode == 1 || gram_mode == 2) ? mtmax : 0;
+  const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
+                         (gram_mode == 1 ? (gc + 7) / 8 : 0);
+  int which = 3;
+  if (aligned) {
     P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
-    if (!impl && try_ws(P, PM, st, e)) {
+    if (try_ws(P, PM, st, e)) {
       if (e != cudaSuccess) {
         set_error("rg_tall_f64: %s", cudaGetErrorString(e));
         return RG_ECUDA;
@@ -1951,38 +1727,34 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
       return RG_OK;
     }
     P.merge12 = 0;
-    int which = 6;
+    which = 6;
     if (a1 + a2 == 0) {
       if (gram_mode == 1)
         which = P.mtiles > 12 ? 6 : 5;  // v5 spills with more than 96 Gram rows; v6<PM, 13> does not
-      else if (gram_mode == 2 && (d_r1 || d_r2))
-        which = 3;
-      else if (gram_mode == 0 && (d_r1 || d_r2) && !getenv("RG_KG_V6"))
-        which = 3;  // CholQR2's two-solve store pass: 0.41 vs 0.44 ms on v6 (profiles/ab_tall_r01.txt)
+      else if (d_r1 || d_r2)
+        which = 3;  // CholQR2 solve passes: 0.41 vs 0.44 ms on v6 (profiles/ab_tall_r01.txt)
     }
-    if (impl) which = impl[0] - '0';
-    const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
-                           (gram_mode == 1 ? (gc + 7) / 8 : 0);
-    if (which == 6 && ncol_slabs <= kMaxSlabs) {
-      P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
-      static const int wide_env = getenv("RG_V6_WIDE") ? atoi(getenv("RG_V6_WIDE")) : 1;
-      const bool wide_ring = wide_env && gram_mode != 1 && PM <= 8 && P.mtiles <= 2 && !d_r1 && !d_r2 && a1 > 0;
-      switch (PM) {
-        RG_V6_CASE(1)
-        RG_V6_CASE(2)
-        RG_V6_CASE(4)
-        RG_V6_CASE(8)
-        RG_V6_CASE(16)
-      }
-    } else if (which != 5) {
-      switch (PM) {
-        RG_V3_CASE(1)
-        RG_V3_CASE(2)
-        RG_V3_CASE(4)
-        RG_V3_CASE(8)
-        RG_V3_CASE(16)
-      }
-    } else
+    if (which == 6 && ncol_slabs > kMaxSlabs) which = 3;
+  }
+  if (which == 6) {
+    P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
+    const bool wide_ring = gram_mode != 1 && PM <= 8 && P.mtiles <= 2 && !d_r1 && !d_r2 && a1 > 0;
+    switch (PM) {
+      RG_V6_CASE(1)
+      RG_V6_CASE(2)
+      RG_V6_CASE(4)
+      RG_V6_CASE(8)
+      RG_V6_CASE(16)
+    }
+  } else if (which == 3) {
+    switch (PM) {
+      RG_V3_CASE(1)
+      RG_V3_CASE(2)
+      RG_V3_CASE(4)
+      RG_V3_CASE(8)
+      RG_V3_CASE(16)
+    }
+  } else {
     switch (PM) {
       RG_V5_CASE(1)
       RG_V5_CASE(2)
@@ -1990,18 +1762,6 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
       RG_V5_CASE(8)
       RG_V5_CASE(16)
     }
-    if (e != cudaSuccess) {
-      set_error("rg_tall_f64: %s", cudaGetErrorString(e));
-      return RG_ECUDA;
-    }
-    return RG_OK;
-  }
-  switch (PM) {
-    RG_TALL_CASE(1)
-    RG_TALL_CASE(2)
-    RG_TALL_CASE(4)
-    RG_TALL_CASE(8)
-    RG_TALL_CASE(16)
   }
   if (e != cudaSuccess) {
     set_error("rg_tall_f64: %s", cudaGetErrorString(e));

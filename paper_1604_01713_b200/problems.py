@@ -149,6 +149,38 @@ def cfg1_sequence():
     return systems, dict(m=20, k=10, tol=1e-8)
 
 
+def cfg3_draws(n: int = 2**24, k: int = 20, p: int = 8, wcols: int = 80, seed: int = 0):
+    """BASELINE configs[2] (block orthogonalization microbench), the raw
+    draws of the reference's recipe in its order (bench.py:110-113,
+    SURVEY.md §8d): one default_rng(seed) gives an n x k N(0,1) block whose
+    thin-QR factor is C, then V (n x p, N(0,1)), then an n x wcols N(0,1)
+    block whose thin-QR factor is the 10-block basis Q.  Returns the three
+    Fortran-ordered draws; ``cfg3_inputs`` orthonormalises them."""
+    rng = np.random.default_rng(seed)
+    Craw = np.asfortranarray(rng.standard_normal((n, k)))
+    V = np.asfortranarray(rng.standard_normal((n, p)))
+    Qraw = np.asfortranarray(rng.standard_normal((n, wcols)))
+    return Craw, V, Qraw
+
+
+def cfg3_inputs(n: int = 2**24, k: int = 20, p: int = 8, wcols: int = 80, seed: int = 0, device=None):
+    """Device-resident cfg3 operands (C, V, Q) as column-major blocks: the
+    draws of ``cfg3_draws`` uploaded once, C and Q orthonormalised by the
+    device thin QR (reduced_qr semantics: r_jj >= 0).  At n = 2^24 the draws
+    take ~20 s on the host and the QRs well under a second on the device."""
+    from . import device as _dev
+    from .dense_kernels import reduced_qr_device
+
+    Craw, V, Qraw = cfg3_draws(n, k, p, wcols, seed)
+    dev = _dev.require_cuda(device)
+    Cd = reduced_qr_device(_dev.to_device_block(Craw, dev)).q
+    del Craw
+    Vd = _dev.to_device_block(V, dev)
+    del V
+    Qd = reduced_qr_device(_dev.to_device_block(Qraw, dev)).q
+    return Cd, Vd, Qd
+
+
 def cfg4_sequence(N: int = 256, n_systems: int = 5, p: int = 8, beta: float = 20.0):
     """BASELINE configs[3]: 3-D conv-diff N^3 (beta=20), p=8 N(0,1) RHS, m=10,
     k=20, tol 1e-8, n_systems systems A_i = A + diag(0.005*i*u*diag(A)),

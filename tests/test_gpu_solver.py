@@ -218,7 +218,7 @@ def test_joint_projection_matches_sequential_cgs2(cuda):
     for joint in (True, False):
         arnoldi.JOINT_PROJECTION = joint
         try:
-            f = arnoldi.start(op.apply, R0, m_max=m, recycle=rs, seed=0)
+            f = arnoldi.start(op.apply, R0, m_max=m, recycle=rs, seed=0, c_orthogonal=True)
             for _ in range(m):
                 arnoldi.step(f, op.apply, recycle=rs)
         finally:

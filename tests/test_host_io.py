@@ -118,3 +118,47 @@ def test_problem_generators_match_kron_recipes():
         assert np.array_equal(np.asarray(A.col_idx), K.indices), name
         assert np.array_equal(A.values, K.data), name
         assert (A.n_rows, A.n_cols) == K.shape, name
+
+
+def test_rgmrecyc_reads_and_writes_reference_files(tmp_path):
+    """A file written by the reference's save_recycle_space
+    (recycling.py:201-209, tests/golden/make_golden_r2.py) loads to the same
+    U and C, and saving them again reproduces the file byte for byte."""
+    from paper_1604_01713_b200.recycling import RecycleSpace, load_recycle_space, save_recycle_space
+
+    g = load_golden("r2_cases.npz")
+    ref_bytes = g["rgmrecyc/bytes"].tobytes()
+    path = tmp_path / "ref.rgm"
+    path.write_bytes(ref_bytes)
+    rs = load_recycle_space(path)  # device blocks on a GPU box, host arrays here
+    u, c = rs.numpy()
+    assert rs.origin == "cross-system"
+    assert np.array_equal(u, g["rgmrecyc/u"]) and np.array_equal(c, g["rgmrecyc/c"])
+    out = tmp_path / "ours.rgm"
+    save_recycle_space(RecycleSpace(u=g["rgmrecyc/u"], c=g["rgmrecyc/c"]), out)
+    assert out.read_bytes() == ref_bytes
+    save_recycle_space(rs, tmp_path / "again.rgm")
+    assert (tmp_path / "again.rgm").read_bytes() == ref_bytes
+    bad = tmp_path / "bad.rgm"
+    bad.write_bytes(b"NOTRECYC" + ref_bytes[8:])
+    with pytest.raises(ValueError, match="not a recycle-space file"):
+        load_recycle_space(bad)
+
+
+def test_progressive_block_ls_vs_reference():
+    """The host progressive least squares (dense_kernels.py:116-203) against
+    the reference's per-step residual norms, Y and R (pls_cases.npz)."""
+    from paper_1604_01713_b200.dense_kernels import ProgressiveBlockLs
+
+    g = load_golden("pls_cases.npz")
+    for case in range(int(g["n"])):
+        H, G0 = g[f"{case}/H"], g[f"{case}/G0"]
+        L, m = int(g[f"{case}/L"]), int(g[f"{case}/m"])
+        pls = ProgressiveBlockLs(L, G0)
+        res = np.array([pls.append_block(H[: (j + 2) * L, j * L:(j + 1) * L]) for j in range(m)])
+        scale = np.abs(G0).max()
+        assert np.abs(res - g[f"{case}/res"]).max() <= 1e-12 * scale, case
+        R = pls.r_factor()
+        assert np.abs(R - g[f"{case}/R"]).max() <= 1e-12 * np.abs(H).max(), case
+        Y = pls.solve()
+        assert np.abs(Y - g[f"{case}/Y"]).max() <= 1e-10 * max(1.0, np.abs(g[f"{case}/Y"]).max()), case

@@ -103,3 +103,47 @@ def test_oracle_ilu0_vs_reference():
         with pytest.raises(oracle.OracleZeroPivot) as e:
             oracle.ilu0(A.indptr, A.indices, A.data)
         assert str(e.value) == str(g[f"err/{key}"])
+
+
+def test_oracle_mgs_step_vs_reference():
+    """Replay each golden block-MGS step (arnoldi.py:159-170) through
+    oracle.mgs_project + oracle.reduced_qr (tests/golden/make_golden_r2.py)."""
+    g = load_golden("r2_cases.npz")
+    for name in ("mgs/plain_n300_L3", "mgs/recyc_n400_L4_k5"):
+        rp, ci, v, shape = csr_from(g, f"{name}/")
+        W, H, F = g[f"{name}/W"], g[f"{name}/H"], g[f"{name}/F"]
+        m, k = int(g[f"{name}/m"]), int(g[f"{name}/k"])
+        L = W.shape[1] // (m + 1)
+        C = g[f"{name}/C"] if k else None
+        scale = np.abs(v).sum()
+        for j in range(m):
+            Ahat = oracle.spmm(rp, ci, v, W[:, j * L:(j + 1) * L])
+            Ahat, Fc, Hc = oracle.mgs_project(Ahat, C, W[:, :(j + 1) * L], L)
+            q, r, flagged = oracle.reduced_qr(Ahat)
+            cols = slice(j * L, (j + 1) * L)
+            assert np.abs(Hc - H[:(j + 1) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            assert np.abs(r - H[(j + 1) * L:(j + 2) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            if k:
+                assert np.abs(Fc - F[:, cols]).max() <= 1e-12 * scale, (name, j)
+            assert not flagged.any()
+            assert np.abs(q - W[:, (j + 1) * L:(j + 2) * L]).max() <= 1e-10, (name, j)
+
+
+def test_oracle_wide_and_unscrubbed_steps_vs_reference():
+    """The r2 CGS2 cases (bases past 128 columns; a recycle space with an
+    R0 that was not projected against C) replay through oracle.arnoldi_step."""
+    g = load_golden("r2_cases.npz")
+    for name in ("unscrubbed", "wide/plain_L8_m20", "wide/recyc_L8_m20_k20"):
+        rp, ci, v, shape = csr_from(g, f"{name}/")
+        W, H, F = g[f"{name}/W"], g[f"{name}/H"], g[f"{name}/F"]
+        m, k = int(g[f"{name}/m"]), int(g[f"{name}/k"])
+        L = W.shape[1] // (m + 1)
+        C = g[f"{name}/C"] if k else None
+        scale = np.abs(v).sum()
+        for j in range(m):
+            q, Fc, Hc, r, flagged = oracle.arnoldi_step(rp, ci, v, W[:, j * L:(j + 1) * L], C, W[:, :(j + 1) * L])
+            cols = slice(j * L, (j + 1) * L)
+            assert np.abs(Hc - H[:(j + 1) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            assert np.abs(r - H[(j + 1) * L:(j + 2) * L, cols]).max() <= 1e-12 * scale, (name, j)
+            if k:
+                assert np.abs(Fc - F[:, cols]).max() <= 1e-12 * scale, (name, j)

@@ -1,6 +1,6 @@
 """Time rg_spmm_csr_c128 at config-5 shape (160^3 complex 27-point stencil)
 and print GB/s of the SpMM model bytes; writes the p=16 output checksum so
-variants (RG_SPMMC_LEGACY / RG_SPMMC_G2_8) can be compared bitwise.
+variant builds (tools/ab_build.py) can be compared bitwise.
 
     python tools/prof_spmm_c128.py [--grid 160] [--p 16,8] [--reps 10]
 """

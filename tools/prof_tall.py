@@ -1,5 +1,5 @@
 """Time one rg_tall configuration in isolation (CUDA events), e.g.
-    RG_TALL_IMPL=3 python tools/prof_tall.py --n 16777216 --p 8 --a1 20 --gc 80
+    python tools/prof_tall.py --n 16777216 --p 8 --a1 20 --gc 80
 """
 import argparse, pathlib, sys
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
