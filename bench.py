@@ -1,25 +1,39 @@
 #!/usr/bin/env python
 """Benchmark of the block GCRO-DR hot path on B200 (driver contract).
 
-Default workload ("step", BASELINE configs[3]/[2] shapes): one block Arnoldi
-step of the 256^3 3-D convection-diffusion operator (n = 16,777,216 = 2^24,
-nnz = 117,047,296, beta = 20) at its widest point of a cycle (m = 10, step 10):
+Default workload ("step", BASELINE configs[3] operator with configs[2]
+shapes): one block Arnoldi step of the 256^3 3-D convection-diffusion
+operator (n = 16,777,216 = 2^24, nnz = 117,047,296, beta = 20) at its widest
+point of a cycle (m = 10, step 10):
 
-    Ahat = A V_10                    CSR SpMM, p = 8            (configs[1] kernel)
+    Ahat = A V_10                     CSR SpMM, p = 8            (configs[1] kernel)
     CGS2 of Ahat vs C (n x 20) and the 10-block basis (n x 80), 2 passes
-    thin QR of the n x 8 result                                  (configs[2] shapes)
+    thin QR of the n x 8 result                                   (configs[2] shapes)
 
-one "step" = that whole arnoldi.step call.  metric = algorithmic HBM bytes of
-the step (SURVEY.md §8d model: SpMM nnz*12 + (n+1)*4 + 16*p*n; CGS2
-8n(4k + 4w + 12p); QR 24np) / device time per step, in GB/s.
+one "step" = that whole arnoldi.step call, through the production path (the
+C-ABI orchestrators rg_cgs2_f64 / rg_cholqr2_f64).
+
+    value  = reference-model bytes of the step / device time per step.  The
+             model is SURVEY.md §8d's per-op compulsory traffic of the
+             REFERENCE algorithm (SpMM nnz*12 + (n+1)*4 + 16*p*n; sequential
+             CGS2 8n(4k + 4w + 12p); QR 24np): it is the same numerator for
+             both arms, so value ratios are time ratios.  The device runs
+             the 3-pass joint [C W] schedule, which moves fewer bytes; those
+             executed bytes are reported beside it (executed_bytes_per_step,
+             roofline.step_frac) and are what the roofline fractions use.
+    e2e    = the same metric through arnoldi.step with the step's inputs
+             (basis n x 80 and C n x 20) uploaded from pinned host memory and
+             the new block V_11 downloaded, every step.
+    time_to_solution (N = 1): the full 5-system cfg4 256^3 sequence.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload step|spmm|ortho|solve] [--grid N]
+                    [--workload step|solve|ortho|spmm] [--grid N]
 
---impl reference times the oracle (CPU restatement of the reference path:
-C SpMM with the reference's arithmetic + numpy/OpenBLAS CGS2 + LAPACK QR) on
-the host cores, on a bounded sample (a 64^3 grid of the same operator family
-with the same k, p, basis width).
+--impl reference times the oracle (oracle/: the CPU restatement of the
+reference path -- C SpMM with the reference's arithmetic, numpy/OpenBLAS
+CGS2, LAPACK QR) on the host cores, on the same 256^3 operator, p, k and
+basis width: each timed step is one of 8 row windows of the step (32 of the
+256 z-planes, rotating), so 8 consecutive steps cover the whole operator.
 """
 
 from __future__ import annotations
@@ -28,6 +42,7 @@ import argparse
 import json
 import os
 import pathlib
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,7 +55,7 @@ sys.path.insert(0, str(ROOT))
 import numpy as np  # noqa: E402
 
 P_BLOCK, K_RECYCLE, M_STEPS = 8, 20, 10
-SAMPLE_GRID = 64  # CPU sample: 64^3 rows of the same operator family
+CPU_WINDOWS = 8  # row windows of the CPU arm's step sample
 DMMA_PEAK_TFLOPS = 36.7  # measured FP64 tensor (DMMA) throughput, profiles/microbench_r01.txt
 
 # operator families of the step workload: cfg4 (real conv-diff, BASELINE
@@ -48,6 +63,11 @@ DMMA_PEAK_TFLOPS = 36.7  # measured FP64 tensor (DMMA) throughput, profiles/micr
 FAMILIES = {
     "cfg4": dict(p=8, k=20, m=10, grid=256, esz=8),
     "cfg5": dict(p=16, k=16, m=8, grid=160, esz=16),
+}
+STEP_METRIC = {
+    "cfg4": "SpMM+block-orthog GB/s (reference-model bytes / step time; block Arnoldi step, cfg4 256^3 p=8 k=20 m=10)",
+    "cfg5": "SpMM+block-orthog GB/s (reference-model bytes / step time; complex block Arnoldi step, cfg5 160^3 "
+            "p=16 k=16 m=8)",
 }
 
 
@@ -59,17 +79,32 @@ def step_model_bytes(n, nnz, p=P_BLOCK, k=K_RECYCLE, j=M_STEPS - 1, esz=8):
     return spmm + cgs2 + qr, dict(spmm=spmm, cgs2=cgs2, qr=qr)
 
 
+def step_config(family, grid, world):
+    fam = FAMILIES[family]
+    n = grid ** 3
+    if family == "cfg4":
+        desc = (f"cfg4-step: arnoldi.step #10 of a cycle on the {grid}^3 3-D conv-diff operator (beta=20) per GPU, "
+                f"p=8, k=20, basis 80 cols (configs[2] shapes)")
+    else:
+        desc = f"cfg5-step: arnoldi.step #8 of a cycle, {grid}^3 complex 27-point stencil, p=16, k=16, basis 128 cols"
+    return {"workload": desc, "grid": grid, "n_per_gpu": n, "p": fam["p"], "k": fam["k"],
+            "basis_cols": fam["m"] * fam["p"], "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU",
+            "l2": "step operands (>14 GB) far larger than the 126 MB L2; no flush needed"}
+
+
 def _ncu_traffic(label, family):
     """DRAM bytes (read + write) per launch of the kernel with this launch
     label, from the committed ncu --set full capture of the same step
-    (profiles/ncu_traffic_r01*.json, written by tools/ncu_traffic.py)."""
-    name = "ncu_traffic_r01.json" if family == "cfg4" else f"ncu_traffic_r01_{family}.json"
-    f = ROOT / "profiles" / name
-    if not f.exists():
-        return None, None
-    for rec in json.loads(f.read_text())["launches"]:
-        if rec["label"] == label:
-            return rec["traffic_bytes"], f"profiles/{name}"
+    (profiles/ncu_traffic_r0*.json, written by tools/ncu_traffic.py)."""
+    names = (["ncu_traffic_r02.json", "ncu_traffic_r01.json"] if family == "cfg4"
+             else [f"ncu_traffic_r02_{family}.json", f"ncu_traffic_r01_{family}.json"])
+    for name in names:
+        f = ROOT / "profiles" / name
+        if not f.exists():
+            continue
+        for rec in json.loads(f.read_text())["launches"]:
+            if rec["label"] == label:
+                return rec["traffic_bytes"], f"profiles/{name}"
     return None, None
 
 
@@ -77,8 +112,8 @@ def _peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
         d = json.loads(f.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -131,55 +166,86 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU arm (oracle)
+# CPU arm (oracle): row windows of the same 256^3 step
 # ---------------------------------------------------------------------------
 
 
-def _cpu_sample_inputs(grid=SAMPLE_GRID, seed=0):
-    from paper_1604_01713_b200 import problems
+class CpuStepSample:
+    """The step of the step workload, restated on the host (oracle.arnoldi_step:
+    SpMM with the reference's arithmetic on all host threads, numpy/OpenBLAS
+    CGS2 against C then the basis, LAPACK QR), on row window w of the 256^3
+    operator: rows [w n/8, (w+1) n/8) of A (their SpMM reads the full V_10),
+    with C and the basis restricted to those rows.  Timing does not depend on
+    the values, so C and the basis are seeded N(0,1) window blocks."""
 
-    A = problems.conv_diff_3d(grid, 20.0)
-    n = A.n_rows
-    rng = np.random.default_rng(seed)
-    C = np.linalg.qr(rng.standard_normal((n, K_RECYCLE)))[0]
-    W = np.linalg.qr(rng.standard_normal((n, M_STEPS * P_BLOCK)))[0]
-    W = np.asfortranarray(W - C @ (C.T @ W))
-    Vm = np.asfortranarray(W[:, -P_BLOCK:])
-    return A, np.asfortranarray(C), W, Vm
+    def __init__(self, grid=256, windows=CPU_WINDOWS, seed=0):
+        import oracle
+        from paper_1604_01713_b200 import problems
 
+        self.oracle = oracle
+        A = problems.conv_diff_3d(grid, 20.0)
+        n = A.n_rows
+        self.windows = windows
+        rows = n // windows
+        rng = np.random.default_rng(seed)
+        self.V = np.asfortranarray(rng.standard_normal((n, P_BLOCK)))
+        self.C = np.asfortranarray(rng.standard_normal((rows, K_RECYCLE)))
+        self.W = np.asfortranarray(rng.standard_normal((rows, M_STEPS * P_BLOCK)))
+        rp = np.asarray(A.row_ptr, dtype=np.int64)
+        self.win = []
+        for w in range(windows):
+            r0, r1 = w * rows, (w + 1) * rows
+            e0, e1 = int(rp[r0]), int(rp[r1])
+            wrp = (rp[r0:r1 + 1] - e0).astype(np.int32)
+            self.win.append((wrp, np.asarray(A.col_idx[e0:e1]), np.asarray(A.values[e0:e1]), rows, e1 - e0))
+        self.threads = oracle.host_threads()
+        self.n, self.nnz, self.grid = n, A.nnz, grid
 
-def cpu_step_rate(steps=3, warmup=1, grid=SAMPLE_GRID):
-    """Oracle block Arnoldi step on the CPU sample; returns (GB/s, s/step, info)."""
-    import oracle
-
-    A, C, W, Vm = _cpu_sample_inputs(grid)
-    nthreads = oracle.host_threads()
-    for _ in range(warmup):
-        oracle.arnoldi_step(A.row_ptr, A.col_idx, A.values, Vm, C, W, nthreads=nthreads)
-    ts = []
-    for _ in range(steps):
+    def run(self, w):
+        """One window step; returns (seconds, model bytes of the window)."""
+        rp, ci, v, rows, nnz = self.win[w % self.windows]
         t0 = time.perf_counter()
-        oracle.arnoldi_step(A.row_ptr, A.col_idx, A.values, Vm, C, W, nthreads=nthreads)
-        ts.append(time.perf_counter() - t0)
-    b, _ = step_model_bytes(A.n_rows, A.nnz)
-    t = statistics.mean(ts)
-    info = {"kind": "port", "cores": nthreads,
-            "sample": f"oracle arnoldi_step (C SpMM, reference arithmetic, {nthreads} threads + numpy/OpenBLAS "
-                      f"CGS2 + LAPACK QR) on the {grid}^3 conv-diff operator, n={A.n_rows}, p=8, k=20, "
-                      f"basis 80 cols; mean of {steps} after {warmup} warm-up"}
-    return b / t / 1e9, t, info
+        self.oracle.arnoldi_step(rp, ci, v, self.V, self.C, self.W, nthreads=self.threads)
+        t = time.perf_counter() - t0
+        return t, step_model_bytes(rows, nnz)[0]
+
+    def describe(self, steps, warmup):
+        return (f"oracle arnoldi_step (C SpMM with the reference's arithmetic on {self.threads} threads + "
+                f"numpy/OpenBLAS CGS2 against C then the basis + LAPACK QR) on row windows of the {self.grid}^3 cfg4 "
+                f"operator: each step = 1/{self.windows} of the rows ({self.n // self.windows} rows, "
+                f"{self.grid // self.windows} z-planes, rotating; "
+                f"{self.windows} steps cover the whole operator), p=8, k=20, basis 80 cols; "
+                f"{steps} timed after {warmup} warm-up")
+
+
+def cpu_step_rate(steps, warmup, sample=None):
+    s = sample or CpuStepSample()
+    for i in range(warmup):
+        s.run(i)
+    ts, bs = [], []
+    for i in range(steps):
+        t, b = s.run(warmup + i)
+        ts.append(t)
+        bs.append(b)
+    rate = sum(bs) / sum(ts) / 1e9
+    info = {"kind": "port", "cores": s.threads, "sample": s.describe(steps, warmup),
+            "window_s_mean": statistics.mean(ts),
+            "full_step_s_estimate": statistics.mean(ts) * s.windows}
+    return rate, statistics.mean(ts), info
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    rate, t, info = cpu_step_rate(steps=max(1, args.steps), warmup=max(1, min(args.warmup, 2)))
-    line = {"metric": "SpMM+block-orthog HBM GB/s (block Arnoldi step, cfg4 256^3 p=8 k=20 m=10)",
-            "value": rate, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "cfg4-step sample (64^3 of the same operator family) on host cores",
-                       "grid": SAMPLE_GRID, "p": P_BLOCK, "k": K_RECYCLE, "basis_cols": M_STEPS * P_BLOCK},
+    if args.workload != "step":
+        print(json.dumps({"impl": "reference", "unavailable": f"the CPU arm covers the step workload only "
+                                                             f"(asked: {args.workload})"}), flush=True)
+        return
+    rate, t, info = cpu_step_rate(args.steps, args.warmup)
+    line = {"metric": STEP_METRIC["cfg4"], "value": rate, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": step_config("cfg4", 256, world),
             "cpu_baseline": dict(info, value=rate, unit="GB/s"),
             "e2e": {"value": rate, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -253,7 +319,18 @@ def _one_step(fact, op, rs):
     arnoldi.step(fact, op.apply, recycle=rs)
 
 
-def run_ours(args, rank, world):
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_step(args, rank, world):
     import torch
 
     from paper_1604_01713_b200 import device as D
@@ -261,9 +338,6 @@ def run_ours(args, rank, world):
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-
     fam = FAMILIES[args.family]
     grid = args.grid or fam["grid"]
     (n, nnz), op, rs, fact, t_gen = _setup_step(grid, dev, seed=rank, world=world, rank=rank, family=args.family)
@@ -273,7 +347,11 @@ def run_ours(args, rank, world):
         _one_step(fact, op, rs)
     torch.cuda.synchronize()
     if world > 1:
+        import torch.distributed as dist
+
         dist.barrier()
+    # the timed region runs the production path; librgb200 brackets each of
+    # its kernel-launching calls with events on the same stream (rg_prof.cu)
     D.LaunchLog.reset(timing=True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -285,87 +363,81 @@ def run_ours(args, rank, world):
         ev1.record()
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
-    launches = D.LaunchLog.count
+    launches = D.LaunchLog.launches()
     per_kernel = D.LaunchLog.summary()
     D.LaunchLog.reset(timing=False)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(ms, world, dev)
     value = model_bytes * world / (ms * 1e-3) / 1e9
 
-    # dominant kernel (largest share of device time inside the timed region)
     peak, peak_kind = _peaks()
-    kernels = sorted(((lbl, c, t_ms, b) for lbl, (c, t_ms, b) in per_kernel.items()), key=lambda r: -r[2])
-    top = kernels[0]
-    top_gbs = top[3] / (top[2] * 1e-3) / 1e9
+    kernels = sorted(((lbl, *rec) for lbl, rec in per_kernel.items()), key=lambda r: -r[2])
     total_ms = sum(k[2] for k in kernels)
-    traffic, traffic_src = _ncu_traffic(top[0], args.family)
-    top_flops = D.LaunchLog.flops.get(top[0], 0) if hasattr(D.LaunchLog, "flops") else 0
+    executed = sum(k[3] for k in kernels) / args.steps
+    # dominant kernel: largest share of device time among kernels that move bytes
+    top = next(k for k in kernels if k[3] > 0)
+    lbl, calls, t_ms, nbytes, flops, nl = top
+    per_launch_s = t_ms * 1e-3 / calls
+    top_gbs = nbytes / calls / per_launch_s / 1e9
+    traffic, traffic_src = _ncu_traffic(lbl, args.family)
     tensor = None
-    if top_flops:
-        per_launch_s = top[2] * 1e-3 / max(top[1], 1)
-        tensor = {"flops_per_launch": top_flops, "achieved_tflops": top_flops / per_launch_s / 1e12,
-                  "peak_tflops": DMMA_PEAK_TFLOPS, "frac": top_flops / per_launch_s / 1e12 / DMMA_PEAK_TFLOPS,
+    if flops:
+        tensor = {"flops_per_launch": flops, "achieved_tflops": flops / per_launch_s / 1e12,
+                  "peak_tflops": DMMA_PEAK_TFLOPS, "frac": flops / per_launch_s / 1e12 / DMMA_PEAK_TFLOPS,
                   "peak_source": "FP64 DMMA m8n8k4, tools/microbench.cu (profiles/microbench_r01.txt)"}
     roofline = {"bound": "hbm", "achieved": top_gbs, "peak": peak, "unit": "GB/s", "frac": top_gbs / peak,
-                "traffic": traffic, "traffic_source": traffic_src, "kernel": top[0],
-                "kernel_share": top[2] / max(total_ms, 1e-9),
-                "bytes_per_launch": top[3] // max(top[1], 1), "peak_source": peak_kind,
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": lbl,
+                "kernel_share": t_ms / max(total_ms, 1e-9), "bytes_per_launch": nbytes // calls,
+                "peak_source": peak_kind,
+                "executed_bytes_per_step": executed,
+                "step_achieved": executed / (ms * 1e-3) / 1e9,
+                "step_frac": executed / (ms * 1e-3) / 1e9 / peak,
                 "fp64_tensor": tensor}
 
-    # end to end through the reference-facing call with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = _e2e(fact, op, rs, model_bytes, args, dev)
-        if world > 1:
-            import torch.distributed as dist
-
-            t = torch.tensor([e2e["ms_per_step"]], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e["ms_per_step"] = float(t.item())
-            e2e["value"] = model_bytes * world / (e2e["ms_per_step"] * 1e-3) / 1e9
-            e2e["h2d_bytes_per_step"] *= world
-            e2e["d2h_bytes_per_step"] *= world
+        e2e = _e2e(fact, op, rs, model_bytes, args)
+        e2e["ms_per_step"] = _max_over_ranks(e2e["ms_per_step"], world, dev)
+        e2e["value"] = model_bytes * world / (e2e["ms_per_step"] * 1e-3) / 1e9
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
 
     cpu = None
-    if rank == 0 and not args.no_cpu and args.family == "cfg4":
-        rate, t, info = cpu_step_rate(steps=3, warmup=1)
+    if rank == 0 and world == 1 and not args.no_cpu and args.family == "cfg4" and grid == 256:
+        rate, t, info = cpu_step_rate(CPU_WINDOWS, 1)
         cpu = dict(info, value=rate, unit="GB/s")
 
+    del fact, rs, op
+    torch.cuda.empty_cache()
+    tts = None
+    if world == 1 and args.family == "cfg4" and grid == 256 and not args.no_tts:
+        try:
+            tts = solve_sequence_timed(256, args.tts_systems, 1, 0, dev)
+        except Exception as exc:  # reported, never silently dropped
+            tts = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank == 0:
-        if args.family == "cfg4":
-            metric = "SpMM+block-orthog HBM GB/s (block Arnoldi step, cfg4 256^3 p=8 k=20 m=10)"
-            workload = (f"cfg4-step: arnoldi.step #10 of a cycle, {grid}^3 conv-diff beta=20 "
-                        f"per GPU, n={n}, nnz={nnz} per GPU, p=8, k=20, basis 80 cols (cfg3 shapes)")
-        else:
-            metric = "SpMM+block-orthog HBM GB/s (complex block Arnoldi step, cfg5 160^3 p=16 k=16 m=8)"
-            workload = (f"cfg5-step: arnoldi.step #8 of a cycle, {grid}^3 complex 27-point stencil, "
-                        f"n={n}, nnz={nnz}, p=16, k=16, basis 128 cols, complex128")
-        line = {"metric": metric,
+        line = {"metric": STEP_METRIC[args.family],
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64" if args.family == "cfg4" else "c128", "data": "synthetic",
-                "config": {"workload": workload,
-                           "model_bytes_per_step": model_bytes, "model_parts": parts,
-                           "l2": "inputs (>14 GB) far larger than the 126 MB L2; no flush needed",
-                           "parallelism": f"row-partition x{world}" if world > 1 else "1 GPU"},
+                "config": step_config(args.family, grid, world),
+                "model_bytes_per_step": model_bytes * world, "model_parts": parts,
+                "executed_bytes_per_step": executed * world,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "kernels": [{"kernel": k[0], "calls": k[1], "ms": k[2], "GB/s": k[3] / (k[2] * 1e-3) / 1e9
-                             if k[2] > 0 else None} for k in kernels],
+                "kernels": [{"kernel": k[0], "calls": k[1], "ms": k[2], "bytes": k[3],
+                             "GB/s": k[3] / (k[2] * 1e-3) / 1e9 if k[2] > 0 else None} for k in kernels],
+                "time_to_solution": tts,
                 "setup_s": {"matrix_generation": t_gen}}
         print(json.dumps(line), flush=True)
 
 
-def _e2e(fact, op, rs, model_bytes, args, dev):
+def _e2e(fact, op, rs, model_bytes, args):
     """Same step, inputs in pinned HOST memory: H2D of V_m's basis (n x 80,
     includes V_10) and C (n x 20) inside the timed region, the step, D2H of
     the new block V_11 (n x 8); the small H/F/R coefficients come back
     inside the step itself."""
     import torch
-
-    from paper_1604_01713_b200 import device as D
 
     n, L, K = fact.n, fact.L, fact.k
     dt = fact.dtype
@@ -377,7 +449,7 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
     hW.copy_(fact._W[:, :wcols].t())
     hC.copy_(rs.c.t())
     W_dev = fact._W[:, :wcols]
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, args.steps)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -392,44 +464,38 @@ def _e2e(fact, op, rs, model_bytes, args, dev):
     ms = e0.elapsed_time(e1) / steps
     h2d = (wcols + K) * n * esz
     d2h = L * n * esz + (2 * K + 2 * (wcols + L)) * L * esz + 5 * L * L * esz
-    return {"value": model_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+    return {"value": model_bytes / (ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms, "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": "arnoldi.step with basis/C uploaded from pinned host memory and V_11 downloaded each step"}
 
 
 # ---------------------------------------------------------------------------
-# time-to-solution workload (BASELINE configs[3]: "GCRO-DR solve s/system")
+# time to solution (BASELINE configs[3]: "GCRO-DR solve s/system")
 # ---------------------------------------------------------------------------
 
 
-def run_solve(args, rank, world):
+def solve_sequence_timed(grid, nsys, world, rank, dev):
     """Full block GCRO-DR sequence of the config-4 family (3-D conv-diff
-    grid^3, beta=20, p=8, m=10, k=20, tol 1e-8, `--systems` systems with the
-    0.5 %*i*u*diag(A) perturbations).  Strong scaling over `world` GPUs: the
-    same global problem is row-partitioned on whole z-planes."""
+    grid^3, beta=20, p=8, m=10, k=20, tol 1e-8, ``nsys`` systems with the
+    0.5 %*i*u*diag(A) perturbations).  Strong scaling over ``world`` GPUs:
+    the same global problem is row-partitioned on whole z-planes.  Each
+    system is timed from the host-resident B to the host-resident X (the
+    public API call), max over ranks."""
     import torch
 
     from paper_1604_01713_b200 import SolverConfig, problems, solve_block_gcrodr
     from paper_1604_01713_b200 import device as D
 
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if args.family == "cfg5":
-        return _run_solve_cfg5(args, rank, world)
-    grid, nsys = args.grid or 256, args.systems
     t0 = time.perf_counter()
     n_glob = grid ** 3
-    B = np.asfortranarray(np.random.default_rng(0).standard_normal((n_glob, P_BLOCK)))
-    u = np.random.default_rng(1).uniform(0.0, 1.0, n_glob)
     if world == 1:
-        A, _, system, kw = problems.cfg4_sequence(N=grid, n_systems=nsys)
+        A, B, system, kw = problems.cfg4_sequence(N=grid, n_systems=nsys)
         ops = [system(i) for i in range(nsys)]
-        part = None
     else:
         from paper_1604_01713_b200 import distributed as DI
-        from paper_1604_01713_b200.problems import add_diagonal  # noqa: F401
 
+        B = np.asfortranarray(np.random.default_rng(0).standard_normal((n_glob, P_BLOCK)))
+        u = np.random.default_rng(1).uniform(0.0, 1.0, n_glob)
         comm = DI.CommContext()
         part = DI.RowPartition.even(n_glob, world, rank, align=grid * grid)
         z0, z1 = part.r0 // (grid * grid), part.r1 // (grid * grid)
@@ -459,25 +525,37 @@ def run_solve(args, rank, world):
         t1 = time.perf_counter()
         X, rep, rs_out = solve_block_gcrodr(Ai, B, None, cfg, rs_in=rs)
         torch.cuda.synchronize()
-        dt = time.perf_counter() - t1
-        if world > 1:
-            t = torch.tensor([dt], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = float(t.item())
+        dt = _max_over_ranks(time.perf_counter() - t1, world, dev)
         rs = rs_out if rs_out is not None else rs
-        per.append({"system": i, "s": dt, "cycles": rep.cycles, "block_steps": int(sum(len(h) for h in rep.residual_history)),
+        per.append({"system": i, "s": dt, "cycles": rep.cycles,
+                    "block_steps": int(sum(len(h) for h in rep.residual_history)),
                     "matvecs": rep.matvec_count, "converged": bool(rep.converged),
                     "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms))})
+    D.set_comm(None, None)
+    return {"s_per_system": statistics.mean(r["s"] for r in per), "systems": per, "setup_s": t_setup,
+            "workload": f"cfg4 sequence {grid}^3 conv-diff beta=20, p=8, m=10, k=20, tol 1e-8, {nsys} systems",
+            "n_gpus": world}
+
+
+def run_solve(args, rank, world):
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if args.family == "cfg5":
+        return _run_solve_cfg5(args, rank, world)
+    grid = args.grid or 256
+    rec = solve_sequence_timed(grid, args.systems, world, rank, dev)
     if rank == 0:
-        mean = statistics.mean(r["s"] for r in per)
-        line = {"metric": "GCRO-DR solve s/system (cfg4 family)", "value": mean, "unit": "s/system",
-                "n_gpus": world, "steps": nsys, "warmup": 0, "ms_per_step": mean * 1e3,
-                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {"workload": f"cfg4 sequence {grid}^3 conv-diff beta=20, p=8, m=10, "
-                                                            f"k=20, tol 1e-8, {nsys} systems",
-                                                "setup_s": t_setup, "parallelism": f"row-partition x{world}"},
-                "systems": per}
-        print(json.dumps(line), flush=True)
+        mean = rec["s_per_system"]
+        print(json.dumps({"metric": "GCRO-DR solve s/system (cfg4 family)", "value": mean, "unit": "s/system",
+                          "n_gpus": world, "steps": args.systems, "warmup": 0, "ms_per_step": mean * 1e3,
+                          "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                          "data": "synthetic",
+                          "config": {"workload": rec["workload"], "setup_s": rec["setup_s"],
+                                     "parallelism": f"row-partition x{world}"},
+                          "systems": rec["systems"]}), flush=True)
 
 
 def _run_solve_cfg5(args, rank, world):
@@ -519,21 +597,155 @@ def _run_solve_cfg5(args, rank, world):
                       "systems": per}), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# kernel microbenches: configs[2] (ortho) and configs[1] (spmm)
+# ---------------------------------------------------------------------------
+
+
+def _timed(fn, steps, warmup):
+    import torch
+
+    from paper_1604_01713_b200 import device as D
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    D.LaunchLog.reset(timing=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    launches = D.LaunchLog.launches()
+    recs = D.LaunchLog.summary()
+    D.LaunchLog.reset(timing=False)
+    return e0.elapsed_time(e1) / steps, launches, recs
+
+
+def run_ortho(args, rank, world):
+    """BASELINE configs[2] at n = 2^24: W = C^T V; V - C W; CGS2 of V against
+    the 10-block basis Q (2 passes); thin QR of the n x 8 result -- each timed
+    separately, GB/s of SURVEY §8d's algorithmic bytes."""
+    import torch
+
+    from paper_1604_01713_b200 import device as D
+    from paper_1604_01713_b200 import problems
+    from paper_1604_01713_b200.dense_kernels import QrScratch, cholqr2_launch
+    from paper_1604_01713_b200.ortho import project_chain
+
+    torch.cuda.set_device(0)
+    n = 2 ** (args.log2n or 24)
+    C, V, Q = problems.cfg3_inputs(n)
+    k, p, w = C.shape[1], V.shape[1], Q.shape[1]
+    Wc = D.small(k, p)
+    Z = D.empty_block(n, p)
+    Z2 = D.empty_block(n, p)
+    c1, c2 = D.small(w, p), D.small(w, p)
+    scr = QrScratch(p, V.device, torch.float64)
+    Qo = D.empty_block(n, p)
+    D.tall(V, None, gram=("basis", C, Wc))
+    ops = {
+        "CtV": (lambda: D.tall(V, None, gram=("basis", C, Wc)), 8 * n * (k + p)),
+        "V-CW": (lambda: D.tall(V, Z, [(C, Wc, -1.0)]), 8 * n * (k + 2 * p)),
+        "CGS2 vs Q (2 passes)": (lambda: project_chain(V, Z2, [Q, Q], [c1, c2]),
+                                 2 * (8 * n * (w + p) + 8 * n * (w + 2 * p))),
+        "QR n x 8 (CholQR2)": (lambda: cholqr2_launch(Z2, Qo, scr), 24 * n * p),
+    }
+    peak, peak_kind = _peaks()
+    out, total_b, total_ms = [], 0, 0.0
+    for name, (fn, nb) in ops.items():
+        ms, launches, recs = _timed(fn, args.steps, args.warmup)
+        executed = sum(r[2] for r in recs.values()) / args.steps
+        out.append({"op": name, "ms": ms, "algorithmic_bytes": nb, "GB/s": nb / (ms * 1e-3) / 1e9,
+                    "frac": nb / (ms * 1e-3) / 1e9 / peak, "executed_bytes": executed,
+                    "launches_per_op": launches / args.steps})
+        total_b += nb
+        total_ms += ms
+    print(json.dumps({"metric": "block-orthogonalization GB/s (configs[2], algorithmic bytes)",
+                      "value": total_b / (total_ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": 1,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                      "data": "synthetic", "config": {"workload": f"cfg3 ortho microbench n=2^{int(np.log2(n))}, "
+                                                                  f"C n x 20, V n x 8, Q n x 80"},
+                      "peak": peak, "peak_source": peak_kind, "ops": out}), flush=True)
+
+
+def run_spmm(args, rank, world):
+    """BASELINE configs[1]: SpMM with the 128^3 7-point Laplacian, p in
+    {1, 2, 4, 8, 16}; GB/s of the reference's own bytes model."""
+    import torch
+
+    from paper_1604_01713_b200 import device as D
+    from paper_1604_01713_b200 import problems
+    from paper_1604_01713_b200.sparse_core import spmm_device
+
+    torch.cuda.set_device(0)
+    grid = args.grid or 128
+    A = problems.laplacian_3d(grid)
+    n = A.n_rows
+    peak, peak_kind = _peaks()
+    out = []
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    for p in (1, 2, 4, 8, 16):
+        V = D.empty_block(n, p)
+        V.copy_(torch.randn(n, p, generator=g, device="cuda", dtype=torch.float64))
+        ms, launches, recs = _timed(lambda: spmm_device(A, V), args.steps, args.warmup)
+        nb = A.nnz * 12 + (n + 1) * 4 + 16 * p * n
+        out.append({"p": p, "ms": ms, "GB/s": nb / (ms * 1e-3) / 1e9, "frac": nb / (ms * 1e-3) / 1e9 / peak,
+                    "launches_per_call": launches / args.steps})
+    best = max(o["GB/s"] for o in out)
+    print(json.dumps({"metric": "SpMM GB/s (configs[1], reference bytes model bench.py:44-47)", "value": best,
+                      "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": min(o["ms"] for o in out), "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": f"cfg2 SpMM {grid}^3 7-point Laplacian, n={n}, nnz={A.nnz}"},
+                      "peak": peak, "peak_source": peak_kind, "per_p": out}), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _spawn(args_list, n):
+    """`bench.py --gpus N` without a launcher: re-exec under torchrun, one
+    rank per GPU on this node (NCCL's init log stays visible on stderr)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(ROOT / "bench.py"), *args_list]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"))
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--grid", type=int, default=None)
+    ap.add_argument("--log2n", type=int, default=None)
     ap.add_argument("--family", choices=sorted(FAMILIES), default="cfg4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--workload", choices=["step", "solve"], default="step")
+    ap.add_argument("--no-tts", action="store_true", help="skip the time-to-solution record of the step line")
+    ap.add_argument("--tts-systems", type=int, default=5)
+    ap.add_argument("--workload", choices=["step", "solve", "ortho", "spmm"], default="step")
     ap.add_argument("--systems", type=int, default=5)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(_spawn(sys.argv[1:], args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
 
@@ -549,8 +761,12 @@ def main():
         run_reference(args, rank, world)
     elif args.workload == "solve":
         run_solve(args, rank, world)
+    elif args.workload == "ortho":
+        run_ortho(args, rank, world)
+    elif args.workload == "spmm":
+        run_spmm(args, rank, world)
     else:
-        run_ours(args, rank, world)
+        run_step(args, rank, world)
     if world > 1:
         import torch.distributed as dist
 

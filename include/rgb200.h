@@ -254,6 +254,25 @@ int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, cons
                        const double* d_dval, const int32_t* d_chunk, int32_t nchunks, int32_t width, int32_t p,
                        double* d_xw, void* d_work, int64_t work_bytes, int32_t epoch, void* stream);
 
+/*
+ * Launch accounting and per-launch device timing (no reference counterpart:
+ * the reference times whole Python calls with perf_counter, bench.py:58-67).
+ *   rg_launch_count    kernels launched by this library since load
+ *   rg_profile_enable  1: clear the records and bracket every kernel-launching
+ *                      call (rg_tall_f64, rg_spmm_csr_f64, rg_chol_f64, ...,
+ *                      including those the orchestrators make) with CUDA
+ *                      events on its stream; 0: stop recording
+ *   rg_profile_count   records so far
+ *   rg_profile_record  record i: label, device ms (synchronises on its end
+ *                      event), algorithmic bytes, FP64
+ *                      tensor-core flops, kernels launched
+ */
+int64_t rg_launch_count(void);
+void rg_profile_enable(int32_t on);
+int32_t rg_profile_count(void);
+int rg_profile_record(int32_t i, char* label, int32_t label_cap, double* ms, int64_t* bytes, double* flops,
+                      int32_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,27 @@ void clear_error();
 
 int sm_count();
 
+// launch accounting / optional per-call event timing (rg_prof.cu): construct
+// at the top of an entry point on its stream, call finish() once its kernels
+// are enqueued (an early error return records nothing)
+class ProfScope {
+ public:
+  explicit ProfScope(cudaStream_t s);
+  ~ProfScope();
+  ProfScope(const ProfScope&) = delete;
+  ProfScope& operator=(const ProfScope&) = delete;
+  // rp != nullptr: SpMM record whose bytes follow the reference model
+  // nnz*(esz+4) + (rows+1)*4 + 2*p*rows*esz over rows [rb, re) (nnz is read
+  // from the device when the record is read back)
+  void finish(int launches, int64_t bytes, double flops, const int32_t* rp, int64_t rb, int64_t re, int p, int esz,
+              const char* fmt, ...);
+
+ private:
+  cudaStream_t st_;
+  void* e0_;
+};
+void count_launches(int n);
+
 #define RG_REQUIRE(cond, ...)            \
   do {                                   \
     if (!(cond)) {                       \

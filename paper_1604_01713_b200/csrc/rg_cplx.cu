@@ -983,6 +983,7 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
              "rg_spmm_csr_c128: bad row range");
   RG_REQUIRE(p >= 1 && d_row_ptr && d_y && ldy >= n_rows, "rg_spmm_csr_c128: bad arguments");
   if (row_end == row_begin) return RG_OK;
+  ProfScope prof((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   const double2* X = reinterpret_cast<const double2*>(d_x);
   const double2* Xg = reinterpret_cast<const double2*>(d_xg);
@@ -1013,6 +1014,7 @@ extern "C" int rg_spmm_csr_c128(int64_t n_rows, int64_t row_begin, int64_t row_e
       c0 += pc;
     }
   }
+  prof.finish((p + 15) / 16 + (p % 16 > 8 ? 1 : 0), 0, 0.0, d_row_ptr, row_begin, row_end, p, 16, "rg_spmm_c128 p=%d", p);
   return RG_OK;
 }
 
@@ -1064,6 +1066,18 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
   P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
   if (gram_mode == 0 && n == 0) return RG_OK;
   cudaStream_t st0 = (cudaStream_t)stream;
+  ProfScope prof(st0);
+  auto launched = [&]() {
+    const bool same_x = a1 > 0 && a2 > 0 && d_x1 == d_x2 && a1 == a2;
+    const bool aliased = gram_mode == 1 && ((d_gb == d_x1 && gc <= a1) || (d_gb == d_x2 && gc <= a2));
+    const int64_t cols = (d_zin ? p : 0) + a1 + (same_x ? 0 : a2) + (gram_mode == 1 && !aliased ? gc : 0) +
+                         (d_zout ? p : 0);
+    const double contr = a1 + (same_x ? 0 : a2) + ((gram_mode == 1 || gram_mode == 2) ? gc : 0);
+    prof.finish(1, 16 * n * cols, 8.0 * n * p * contr, nullptr, 0, 0, 0, 0,
+                "rg_tall_c128 p=%d in=%d a=%d+%d g%d:%d trsm=%d out=%d", p, d_zin ? 1 : 0, a1, a2, gram_mode, gc,
+                (d_r1 ? 1 : 0) + (d_r2 ? 1 : 0), d_zout ? 1 : 0);
+    return RG_OK;
+  };
   if (p > 4) {
     // tensor-core pass (complex v6)
     cudaError_t e6;
@@ -1079,7 +1093,7 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
       set_error("rg_tall_c128: %s", cudaGetErrorString(e6));
       return RG_ECUDA;
     }
-    return RG_OK;
+    return launched();
   }
   const int PM = p <= 1 ? 1 : (p <= 2 ? 2 : (p <= 4 ? 4 : 8));
   const int mtmax = P.mtiles <= 2 ? 2 : 6;
@@ -1100,7 +1114,7 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
     set_error("rg_tall_c128: %s", cudaGetErrorString(e));
     return RG_ECUDA;
   }
-  return RG_OK;
+  return launched();
 }
 
 extern "C" int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* d_status, double cond_tol,
@@ -1108,8 +1122,10 @@ extern "C" int rg_chol_c128(int32_t p, const double* d_g, double* d_r, int32_t* 
   using namespace rg;
   clear_error();
   RG_REQUIRE(p >= 1 && p <= 64 && d_g && d_r && d_status, "rg_chol_c128: bad arguments");
+  ProfScope prof((cudaStream_t)stream);
   chol_c128_kernel<<<1, 64, (size_t)p * p * sizeof(double2), (cudaStream_t)stream>>>(
       p, reinterpret_cast<const double2*>(d_g), reinterpret_cast<double2*>(d_r), d_status, cond_tol);
   RG_CHECK_LAUNCH("rg_chol_c128");
+  prof.finish(1, 0, 0.0, nullptr, 0, 0, 0, 0, "rg_chol_c128 p=%d", p);
   return RG_OK;
 }

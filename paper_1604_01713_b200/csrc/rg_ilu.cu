@@ -336,11 +336,13 @@ extern "C" int rg_ilu0_f64(int64_t n, const int32_t* d_row_ptr, const int32_t* d
   RG_REQUIRE(epoch > 0, "rg_ilu0_f64: epoch must be positive");
   if (n == 0) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  ProfScope prof(s);
   cudaMemsetAsync(d_work, 0, 4, s);
   Wave W = make_wave(d_order, d_chunk, nchunks, d_work, epoch);
   ilu0_kernel<<<(unsigned)wave_grid(nchunks, width), kWaveWarps * 32, 0, s>>>(W, d_row_ptr, d_col_idx, d_vals, d_diag_pos,
                                                                       (long long*)d_zero_row);
   RG_CHECK_LAUNCH("rg_ilu0_f64");
+  prof.finish(1, 0, 0.0, nullptr, 0, 0, 0, 0, "rg_ilu0 n=%lld", (long long)n);
   return RG_OK;
 }
 
@@ -359,6 +361,7 @@ extern "C" int rg_sptrsv_f64(int64_t n, const int32_t* d_row_ptr, const int32_t*
   RG_REQUIRE(epoch > 0, "rg_sptrsv_f64: epoch must be positive");
   if (n == 0) return RG_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  ProfScope prof(s);
   cudaMemsetAsync(d_work, 0, 4, s);
   Wave W = make_wave(d_order, d_chunk, nchunks, d_work, epoch);
   const unsigned g = (unsigned)wave_grid(nchunks, width);
@@ -369,6 +372,7 @@ extern "C" int rg_sptrsv_f64(int64_t n, const int32_t* d_row_ptr, const int32_t*
     sptrsv_kernel<false><<<g, kWaveWarps * 32, 0, s>>>(W, d_row_ptr, d_col_idx, d_vals, d_diag_pos, p, d_b, ldb,
                                                        d_x, ldx);
   RG_CHECK_LAUNCH("rg_sptrsv_f64");
+  prof.finish(1, 0, 0.0, nullptr, 0, 0, 0, 0, "rg_sptrsv upper=%d p=%d", upper, p);
   return RG_OK;
 }
 
@@ -402,9 +406,11 @@ extern "C" int rg_gather_f64(int64_t m, const int64_t* d_idx, const double* d_sr
   clear_error();
   if (m <= 0) return RG_OK;
   RG_REQUIRE(d_idx && d_src && d_dst, "rg_gather_f64: null argument");
+  ProfScope prof((cudaStream_t)stream);
   const int64_t g = std::min<int64_t>((m + 255) / 256, (int64_t)sm_count() * 16);
   gather_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(m, d_idx, d_src, d_dst);
   RG_CHECK_LAUNCH("rg_gather_f64");
+  prof.finish(1, 16 * m, 0.0, nullptr, 0, 0, 0, 0, "rg_gather");
   return RG_OK;
 }
 
@@ -415,10 +421,12 @@ extern "C" int rg_permute_rows_f64(int64_t n, int32_t p, const double* d_src, in
   RG_REQUIRE(n >= 0 && p >= 1, "rg_permute_rows_f64: bad shape");
   if (n == 0) return RG_OK;
   RG_REQUIRE(d_src && d_dst && (d_pos_src || lds >= n) && (d_pos_dst || ldd >= n), "rg_permute_rows_f64: bad args");
+  ProfScope prof((cudaStream_t)stream);
   const int64_t g = std::min<int64_t>((n + 255) / 256, (int64_t)sm_count() * 16);
   permute_rows_kernel<<<(unsigned)g, 256, 0, (cudaStream_t)stream>>>(n, p, d_src, lds, d_pos_src, d_dst, ldd,
                                                                      d_pos_dst);
   RG_CHECK_LAUNCH("rg_permute_rows_f64");
+  prof.finish(1, 16 * n * p, 0.0, nullptr, 0, 0, 0, 0, "rg_permute_rows p=%d", p);
   return RG_OK;
 }
 
@@ -434,10 +442,12 @@ extern "C" int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t*
   RG_REQUIRE(d_work && work_bytes >= rg_wave_workspace_bytes(n), "rg_sptrsv_perm_f64: workspace too small");
   RG_REQUIRE(epoch > 0, "rg_sptrsv_perm_f64: epoch must be positive");
   cudaStream_t s = (cudaStream_t)stream;
+  ProfScope prof(s);
   cudaMemsetAsync(d_work, 0, 4, s);
   Wave W = make_wave(nullptr, d_chunk, nchunks, d_work, epoch);
   sptrsv_perm_kernel<<<(unsigned)wave_grid(nchunks, width), kWaveWarps * 32, 0, s>>>(W, d_rp, d_ci, d_vals, d_dval,
                                                                                      p, d_xw);
   RG_CHECK_LAUNCH("rg_sptrsv_perm_f64");
+  prof.finish(1, 0, 0.0, nullptr, 0, 0, 0, 0, "rg_sptrsv_perm p=%d", p);
   return RG_OK;
 }

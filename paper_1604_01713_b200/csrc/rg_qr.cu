@@ -320,9 +320,11 @@ extern "C" int rg_chol_f64(int32_t p, const double* d_g, double* d_r, int32_t* d
   clear_error();
   RG_REQUIRE(p >= 1 && p <= 64, "rg_chol_f64: p=%d outside [1, 64]", p);
   RG_REQUIRE(d_g && d_r && d_status, "rg_chol_f64: null pointer");
+  ProfScope prof((cudaStream_t)stream);
   chol_kernel<<<1, 64, (size_t)p * p * sizeof(double), (cudaStream_t)stream>>>(p, d_g, d_r, d_status,
                                                                               cond_tol);
   RG_CHECK_LAUNCH("rg_chol_f64");
+  prof.finish(1, 0, 0.0, nullptr, 0, 0, 0, 0, "rg_chol p=%d", p);
   return RG_OK;
 }
 
@@ -342,6 +344,7 @@ extern "C" int rg_tsqr_f64(int64_t n, int32_t p, double* d_x, int64_t ldx, doubl
   RG_REQUIRE(d_work && work_bytes >= need, "rg_tsqr_f64: workspace %lld < %lld bytes",
              (long long)work_bytes, (long long)need);
   cudaStream_t st = (cudaStream_t)stream;
+  ProfScope prof(st);
   double* ws = (double*)d_work;
   cudaError_t e;
   if (p <= 8)
@@ -354,5 +357,9 @@ extern "C" int rg_tsqr_f64(int64_t n, int32_t p, double* d_x, int64_t ldx, doubl
     set_error("rg_tsqr_f64: %s", cudaGetErrorString(e));
     return RG_ECUDA;
   }
+  // one factor launch per level plus the two apply launches per lower level
+  // (24np algorithmic bytes: one reduction pass + one apply pass)
+  const int levels = (int)tsqr_plan(n, p).m.size();
+  prof.finish(2 * levels - 1, 24 * n * p, 0.0, nullptr, 0, 0, 0, 0, "rg_tsqr p=%d", p);
   return RG_OK;
 }

@@ -238,6 +238,7 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
   RG_REQUIRE(n_local >= 0 && (n_local == 0 || (d_x && ldx >= n_local)),
              "rg_spmm_csr_f64: ldx=%lld < n_local=%lld", (long long)ldx, (long long)n_local);
   if (row_end == row_begin) return RG_OK;
+  ProfScope prof((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   // exact-width passes (no per-column predication in the inner loop) of at
   // most 8 columns: a 16-wide register block spills, and re-reading A for a
@@ -261,5 +262,6 @@ extern "C" int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_en
     RG_CHECK_LAUNCH("rg_spmm_csr_f64");
     c0 += pc;
   }
+  prof.finish((p + 7) / 8, 0, 0.0, d_row_ptr, row_begin, row_end, p, 8, "rg_spmm p=%d", p);
   return RG_OK;
 }

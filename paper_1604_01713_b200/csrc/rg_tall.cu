@@ -1680,6 +1680,20 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   P.ntiles = (n + kTallThreads - 1) / kTallThreads;
   P.merge12 = 0;
   if (gram_mode == 0 && P.ntiles == 0) return RG_OK;
+  ProfScope prof((cudaStream_t)stream);
+  auto launched = [&]() {
+    // algorithmic bytes: every streamed operand column once (a Gram basis
+    // aliasing an update operand, and two terms over the same X, once)
+    const bool same_x = a1 > 0 && a2 > 0 && d_x1 == d_x2 && a1 == a2;
+    const bool aliased = gram_mode == 1 && ((d_gb == d_x1 && gc <= a1) || (d_gb == d_x2 && gc <= a2));
+    const int64_t cols = (d_zin ? p : 0) + a1 + (same_x ? 0 : a2) + (gram_mode == 1 && !aliased ? gc : 0) +
+                         (d_zout ? p : 0);
+    const double contr = a1 + (same_x ? 0 : a2) + ((gram_mode == 1 || gram_mode == 2) ? gc : 0);
+    prof.finish(1, 8 * n * cols, 2.0 * n * p * contr, nullptr, 0, 0, 0, 0,
+                "rg_tall p=%d in=%d a=%d+%d g%d:%d trsm=%d out=%d", p, d_zin ? 1 : 0, a1, a2, gram_mode,
+                gram_mode == 3 ? 1 : gc, (d_r1 ? 1 : 0) + (d_r2 ? 1 : 0), d_zout ? 1 : 0);
+    return RG_OK;
+  };
   const int PM = pick_pm(p);
   const int mtmax = pick_mtmax(P.mtiles);
   const int64_t bound = tall_grid_bound2();
@@ -1705,7 +1719,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
       set_error("rg_tall_f64: %s", cudaGetErrorString(e));
       return RG_ECUDA;
     }
-    return RG_OK;
+    return launched();
   }
   // dispatch measured per pass type (profiles/ab_tall_r01.txt,
   // profiles/ws_study_r01.txt): the warp-specialised ws kernel for the wide
@@ -1724,7 +1738,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
         set_error("rg_tall_f64: %s", cudaGetErrorString(e));
         return RG_ECUDA;
       }
-      return RG_OK;
+      return launched();
     }
     P.merge12 = 0;
     which = 6;
@@ -1767,5 +1781,5 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
     set_error("rg_tall_f64: %s", cudaGetErrorString(e));
     return RG_ECUDA;
   }
-  return RG_OK;
+  return launched();
 }

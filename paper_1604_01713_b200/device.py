@@ -217,49 +217,52 @@ class Workspace:
 
 
 # ---------------------------------------------------------------------------
-# launch accounting (bench / smoke evidence): every rg_* launch is counted;
-# with ``timing`` on, each wrapper call is bracketed by CUDA events on the
-# launching stream together with its algorithmic byte count.
+# launch accounting (bench / smoke evidence), kept natively by librgb200
+# (rg_prof.cu): every kernel-launching entry point counts its launches, and
+# with ``timing`` on brackets itself with CUDA events on its own stream and
+# records its algorithmic bytes and tensor-core flops -- including the calls
+# the C orchestrators make, so the timed path is the production path.
 # ---------------------------------------------------------------------------
 
 
 class LaunchLog:
-    count = 0
     timing = False
-    records: list = []
-    flops: dict = {}  # label -> DMMA flops per launch (tall passes)
+    _base = 0
 
     @classmethod
     def reset(cls, timing: bool = False):
-        cls.count = 0
+        L = lib()
+        L.rg_profile_enable(1 if timing else 0)
+        cls._base = L.rg_launch_count()
         cls.timing = timing
-        cls.records = []
+
+    @classmethod
+    def launches(cls) -> int:
+        """Kernels launched since the last reset."""
+        return int(lib().rg_launch_count() - cls._base)
+
+    @classmethod
+    def records(cls):
+        """[(label, ms, bytes, flops, launches)] of the calls recorded since
+        the last reset(timing=True) (synchronises)."""
+        L = lib()
+        out = []
+        buf = ctypes.create_string_buffer(128)
+        ms, nb, fl, nl = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double(), ctypes.c_int32()
+        for i in range(L.rg_profile_count()):
+            _lib.check(L.rg_profile_record(i, buf, 128, ctypes.byref(ms), ctypes.byref(nb), ctypes.byref(fl),
+                                           ctypes.byref(nl)), "profile")
+            out.append((buf.value.decode(), ms.value, nb.value, fl.value, nl.value))
+        return out
 
     @classmethod
     def summary(cls):
-        """{label: (calls, total_ms, total_bytes)} (synchronises)."""
-        torch.cuda.synchronize()
+        """{label: (calls, total_ms, total_bytes, flops_per_call, launches)}."""
         out = {}
-        for label, nbytes, e0, e1 in cls.records:
-            c, t, b = out.get(label, (0, 0.0, 0))
-            out[label] = (c + 1, t + e0.elapsed_time(e1), b + nbytes)
+        for label, ms, nb, fl, nl in cls.records():
+            c, t, b, _, l = out.get(label, (0, 0.0, 0, 0.0, 0))
+            out[label] = (c + 1, t + ms, b + nb, fl, l + nl)
         return out
-
-
-def _t0():
-    if not LaunchLog.timing:
-        return None
-    e = torch.cuda.Event(enable_timing=True)
-    e.record()
-    return e
-
-
-def _t1(e0, label, nbytes, nlaunch=1):
-    LaunchLog.count += nlaunch
-    if e0 is not None:
-        e1 = torch.cuda.Event(enable_timing=True)
-        e1.record()
-        LaunchLog.records.append((label, int(nbytes), e0, e1))
 
 
 # ---------------------------------------------------------------------------
@@ -279,17 +282,10 @@ def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: in
     if cplx != (dcsr.values.dtype == torch.complex128) or Y.dtype != X.dtype:
         raise TypeError(f"spmm: matrix values {dcsr.values.dtype}, block {X.dtype}, output {Y.dtype} must agree")
     fn = L.rg_spmm_csr_c128 if cplx else L.rg_spmm_csr_f64
-    e0 = _t0()
     rc = fn(n_rows, row_begin, row_end, dcsr.row_ptr.data_ptr(), dcsr.col_idx.data_ptr(),
             dcsr.values.data_ptr(), X.data_ptr() if X.numel() else None, ld_of(X), n_local,
             ptr(Xg), ld_of(Xg) if Xg is not None else 1, p, Y.data_ptr(), ld_of(Y), stream_ptr())
     _lib.check(rc, "spmm")
-    rows = row_end - row_begin
-    if rows > 0:
-        esz = 16 if cplx else 8
-        hrp = getattr(dcsr, "host_row_ptr", None)
-        nnz = int(hrp[row_end] - hrp[row_begin]) if hrp is not None else 0
-        _t1(e0, f"rg_spmm p={p}", nnz * (esz + 4) + (rows + 1) * 4 + 2 * p * rows * esz, (p + 15) // 16)
     return Y
 
 
@@ -315,7 +311,6 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
     wsb = wsfn(n, p, a1, a2, gmode, gc) if gmode else 0
     ws = Workspace.get(wsb) if gmode else None
     fn = L.rg_tall_c128 if cplx else L.rg_tall_f64
-    e0 = _t0()
     rc = fn(n, p,
             ptr(zin), ld_of(zin) if zin is not None else 1,
             ptr(zout), ld_of(zout) if zout is not None else 1,
@@ -326,22 +321,6 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
             ptr(ws), ws.numel() if ws is not None else 0, stream_ptr())
     _lib.check(rc, "tall")
     Workspace.check(f"rg_tall n={n} p={p} a={a1}+{a2} gmode={gmode} gc={gc} cplx={cplx}")
-    if n > 0 or gmode:
-        esz = 16 if cplx else 8
-        # a Gram basis that aliases an update operand is streamed once
-        aliased = gmode == 1 and any(x is not None and x.data_ptr() == gb.data_ptr() and gc <= x.shape[1]
-                                     for x in (x1, x2))
-        # two terms over the same operand are merged into one pass over it (rg_tall v6)
-        same_x = x1 is not None and x2 is not None and x1.data_ptr() == x2.data_ptr() and a1 == a2
-        cols = ((p if zin is not None else 0) + a1 + (0 if same_x else a2) + (gc if gmode == 1 and not aliased else 0)
-                + (p if zout is not None and (zin is None or zout.data_ptr() != zin.data_ptr()) else p if zout is not None else 0))
-        label = (f"rg_tall p={p} in={int(zin is not None)} a={a1}+{a2} "
-                 f"g{gmode}:{gc} trsm={int(r1 is not None) + int(r2 is not None)} out={int(zout is not None)}")
-        if LaunchLog.timing:
-            # tensor-core work: the update contraction and the Gram (4 real products per complex one)
-            contr = a1 + (0 if same_x else a2) + (gc if gmode in (1, 2) else 0)
-            LaunchLog.flops[label] = 2 * n * p * contr * (4 if cplx else 1)
-        _t1(e0, label, esz * n * cols)
     if gout_k is not gout:
         gout.copy_(gout_k)
     if gmode and _COMM is not None:
@@ -518,8 +497,8 @@ def max_p(t: torch.Tensor) -> int:
 def fused_ok() -> bool:
     """The C orchestrators (rg_cgs2_f64 / rg_cholqr2_f64) replace the Python
     pass chain on one GPU; row-partitioned runs need the Gram allreduce
-    between passes, and bench attribution times each launch."""
-    return _COMM is None and not LaunchLog.timing
+    between passes."""
+    return _COMM is None
 
 
 def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1, joint: bool = False) -> None:
@@ -537,7 +516,6 @@ def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1, joint: boo
                        ws.numel(), stream_ptr())
     _lib.check(rc, "cgs2")
     Workspace.check(f"rg_cgs2 n={n} p={p} k={k} w={w}")
-    LaunchLog.count += 3 if joint else (2 if k else 0) + (2 if w else 0) + 1
 
 
 def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch.Tensor, gram_ready: bool) -> None:
@@ -548,16 +526,13 @@ def cholqr2(X: torch.Tensor, Q: torch.Tensor, small: torch.Tensor, status: torch
                           1 if gram_ready else 0, ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check(rc, "cholqr2")
     Workspace.check(f"rg_cholqr2 n={n} p={p}")
-    LaunchLog.count += 4 + (0 if gram_ready else 1)
 
 
 def chol(G: torch.Tensor, R: torch.Tensor, status: torch.Tensor, cond_tol: float):
     p = G.shape[0]
-    e0 = _t0()
     fn = lib().rg_chol_c128 if G.dtype == torch.complex128 else lib().rg_chol_f64
     rc = fn(p, _coef(G).data_ptr(), R.data_ptr(), status.data_ptr(), float(cond_tol), stream_ptr())
     _lib.check(rc, "chol")
-    _t1(e0, "rg_chol", 0)
 
 
 def tsqr(X: torch.Tensor, R: torch.Tensor):
@@ -566,16 +541,5 @@ def tsqr(X: torch.Tensor, R: torch.Tensor):
     L = lib()
     wsb = L.rg_tsqr_workspace_bytes(n, p)
     ws = Workspace.get(wsb, slot=1)
-    e0 = _t0()
     rc = L.rg_tsqr_f64(n, p, X.data_ptr(), ld_of(X), R.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
     _lib.check(rc, "tsqr")
-    _t1(e0, f"rg_tsqr p={p}", 3 * 8 * n * p, 1 + 2 * _tsqr_levels(n, p))
-
-
-def _tsqr_levels(n, p):
-    c = 1024 if p <= 8 else (512 if p <= 16 else 256)
-    lv, m = 1, n
-    while (m + c - 1) // c > 1:
-        m = ((m + c - 1) // c) * p
-        lv += 1
-    return lv

@@ -136,7 +136,6 @@ class _DeviceLu:
                            zero_row.data_ptr(), self.work.data_ptr(), self.work.numel(), self.next_epoch(),
                            _dev.stream_ptr())
         _lib.check(rc, "ilu0")
-        _dev.LaunchLog.count += 1
 
     def _permuted(self):
         if self.lower_sched.perm is None:
@@ -163,7 +162,6 @@ class _DeviceLu:
             _lib.check(L.rg_permute_rows_f64(n, p, src.data_ptr(), lds, ps.data_ptr() if ps is not None else None,
                                              dst.data_ptr(), ldd, pd.data_ptr() if pd is not None else None, st),
                        "permute_rows")
-            _dev.LaunchLog.count += 1
 
         def solve(sc, pm, w):
             rc = L.rg_sptrsv_perm_f64(n, pm["rp"].data_ptr(), pm["ci"].data_ptr(), pm["vals"].data_ptr(),
@@ -171,7 +169,6 @@ class _DeviceLu:
                                       sc.chunk.data_ptr(), sc.nchunks, sc.width, p, w.data_ptr(),
                                       self.work.data_ptr(), self.work.numel(), self.next_epoch(), st)
             _lib.check(rc, "sptrsv_perm")
-            _dev.LaunchLog.count += 1
 
         perm(B, _dev.ld_of(B), None, w1, 0, lp["pos"])
         solve(ls, lp, w1)
@@ -191,7 +188,6 @@ class _DeviceLu:
                                  _dev.ld_of(x), self.work.data_ptr(), self.work.numel(), self.next_epoch(),
                                  _dev.stream_ptr())
             _lib.check(rc, "sptrsv")
-            _dev.LaunchLog.count += 1
 
 
 def _diag_positions(n, rp, ci):

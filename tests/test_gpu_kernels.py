@@ -168,8 +168,8 @@ def test_tall_wide_terms_and_gram_split(cuda):
     ref = Z.copy()
     for X, S in zip(Xs, Ss):
         ref = ref - X @ S
-    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-11
-    assert _rel(out.cpu().numpy(), Gb.T @ ref) <= 1e-11
+    assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
+    assert _rel(out.cpu().numpy(), Gb.T @ ref) <= 1e-12
 
 
 @pytest.mark.parametrize("n", [5, 64, 1000, 70001])
@@ -232,7 +232,7 @@ def test_tall_passes_ignore_padding_rows(cuda):
             assert _rel(D.to_numpy_block(Zo), z) <= 1e-12
             if gmode:
                 ref = (X if alias else Gb).T @ z if gmode == 1 else z.T @ z
-                assert np.isfinite(G.cpu().numpy()).all() and _rel(G.cpu().numpy(), ref) <= 1e-11
+                assert np.isfinite(G.cpu().numpy()).all() and _rel(G.cpu().numpy(), ref) <= 1e-12
 
 
 def test_tall_empty_rows(cuda):
@@ -282,7 +282,7 @@ def test_reduced_qr_golden(cuda):
         assert np.abs(f.r_factor[:j0, :] - r_ref[:j0, :]).max(initial=0.0) <= tol, name
         assert np.all(np.diagonal(f.r_factor) >= 0.0)
         q = f.q
-        assert np.abs(q[:, :j0] - g[f"{name}/q"][:, :j0]).max(initial=0.0) <= 1e-11 * max(cond, 1.0), name
+        assert np.abs(q[:, :j0] - g[f"{name}/q"][:, :j0]).max(initial=0.0) <= 1e-12 * max(cond, 1.0), name
         assert np.linalg.norm(q.T @ q - np.eye(q.shape[1])) <= 1e-12 * q.shape[1]
         assert np.linalg.norm(q @ f.r_factor - X) <= 1e-13 * max(np.linalg.norm(X), 1e-300) * X.shape[1]
 
@@ -341,7 +341,7 @@ def test_reduced_qr_wide_blocks(cuda, L):
     assert not f.flagged.any()
     assert _rel(f.r_factor, r_ref) <= 1e-12 * np.linalg.cond(X)
     assert np.linalg.norm(f.q.T @ f.q - np.eye(L)) <= 1e-13 * L
-    assert np.abs(f.q - q_ref).max() <= 1e-11
+    assert np.abs(f.q - q_ref).max() <= 1e-12
 
 
 def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
@@ -372,9 +372,9 @@ def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
     c1 = hc[k * p:(k + w) * p].reshape(p, w).T
     S2 = hc[(k + w) * p:(2 * k + w) * p].reshape(p, k).T
     c2 = hc[(2 * k + w) * p:].reshape(p, w).T
-    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12 * 1e3
-    assert np.abs(S1 + S2 - F).max() <= 1e-12 * np.abs(F).max() * 10
-    assert np.abs(c1 + c2 - H).max() <= 1e-12 * np.abs(H).max() * 10
+    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12
+    assert np.abs(S1 + S2 - F).max() <= 1e-12 * np.abs(F).max()
+    assert np.abs(c1 + c2 - H).max() <= 1e-12 * np.abs(H).max()
     Qd = D.empty_block(n, p)
     status = torch.zeros(2, dtype=torch.int32, device=cuda)
     rc = L.rg_cholqr2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), Qd.data_ptr(), D.ld_of(Qd), small.data_ptr(),
@@ -383,8 +383,8 @@ def test_c_abi_cgs2_and_cholqr2_entry_points(cuda):
     sm = small.cpu().numpy().reshape(4, p, p).transpose(0, 2, 1)
     R = np.triu(sm[3] @ sm[1])
     q_ref, r_ref, _ = oracle.reduced_qr(ref)
-    assert _rel(R, r_ref) <= 1e-11
-    assert np.abs(D.to_numpy_block(Qd) - q_ref).max() <= 1e-10
+    assert _rel(R, r_ref) <= 1e-12 * np.linalg.cond(r_ref)
+    assert np.abs(D.to_numpy_block(Qd) - q_ref).max() <= 1e-12 * np.linalg.cond(r_ref)
 
 
 def test_c_abi_cgs2_joint_schedule(cuda):
@@ -407,12 +407,12 @@ def test_c_abi_cgs2_joint_schedule(cuda):
     rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), CW.data_ptr(), D.ld_of(CW), k, CW[:, k:].data_ptr(),
                        D.ld_of(CW), w, coef.data_ptr(), None, 1, ws.data_ptr(), ws.numel(), D.stream_ptr())
     assert rc == 0
-    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12 * 1e3
+    assert _rel(D.to_numpy_block(Zd), ref) <= 1e-12
     hc = coef.cpu().numpy()
     G1 = hc[: (k + w) * p].reshape(p, k + w).T
     G2 = hc[(k + w) * p:].reshape(p, k + w).T
-    assert np.abs((G1 + G2)[:k] - F).max() <= 1e-11 * max(1.0, np.abs(F).max())
-    assert np.abs((G1 + G2)[k:] - H).max() <= 1e-11 * max(1.0, np.abs(H).max())
+    assert np.abs((G1 + G2)[:k] - F).max() <= 1e-12 * max(1.0, np.abs(F).max())
+    assert np.abs((G1 + G2)[k:] - H).max() <= 1e-12 * max(1.0, np.abs(H).max())
     Wsep = D.to_device_block(Q[:, k:])
     rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), CW.data_ptr(), D.ld_of(CW), k, Wsep.data_ptr(),
                        D.ld_of(Wsep), w, coef.data_ptr(), None, 1, ws.data_ptr(), ws.numel(), D.stream_ptr())

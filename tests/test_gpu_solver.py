@@ -39,11 +39,13 @@ def test_arnoldi_golden(cuda):
         for _ in range(m):
             arnoldi.step(fact, op.apply, recycle=rs)
         scale = A.frobenius_norm()
-        assert np.abs(fact.h_bar - g[f"{name}/H"]).max() <= 1e-10 * scale, name
+        # measured on B200: H, F within ~2e-15 ||A||_F, W within ~1e-14
+        # (gpurun_out/parity.jsonl via tests/parity_log.py)
+        assert np.abs(fact.h_bar - g[f"{name}/H"]).max() <= 1e-12 * scale, name
         assert np.abs(fact.z_bar - g[f"{name}/z_bar"]).max() <= 1e-12 * np.abs(g[f"{name}/z_bar"]).max(), name
         if k:
-            assert np.abs(fact.f - g[f"{name}/F"]).max() <= 1e-10 * scale, name
-        assert np.abs(fact.w_numpy() - g[f"{name}/W"]).max() <= 1e-9, name
+            assert np.abs(fact.f - g[f"{name}/F"]).max() <= 1e-12 * scale, name
+        assert np.abs(fact.w_numpy() - g[f"{name}/W"]).max() <= 1e-12, name
         assert len(fact.breakdown_events) == int(g[f"{name}/events"]), name
         # exact block-Hessenberg zeros and nonnegative closing diagonals
         H, L = fact.h_bar, fact.L
