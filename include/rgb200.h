@@ -258,6 +258,8 @@ int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, cons
  * Launch accounting and per-launch device timing (no reference counterpart:
  * the reference times whole Python calls with perf_counter, bench.py:58-67).
  *   rg_launch_count    kernels launched by this library since load
+ *   rg_count_launches  add n (a host replaying a captured CUDA graph of
+ *                      library calls reports the kernels each replay runs)
  *   rg_profile_enable  1: clear the records and bracket every kernel-launching
  *                      call (rg_tall_f64, rg_spmm_csr_f64, rg_chol_f64, ...,
  *                      including those the orchestrators make) with CUDA
@@ -268,6 +270,7 @@ int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, cons
  *                      tensor-core flops, kernels launched
  */
 int64_t rg_launch_count(void);
+void rg_count_launches(int64_t n);
 void rg_profile_enable(int32_t on);
 int32_t rg_profile_count(void);
 int rg_profile_record(int32_t i, char* label, int32_t label_cap, double* ms, int64_t* bytes, double* flops,

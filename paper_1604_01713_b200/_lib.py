@@ -63,6 +63,7 @@ PROTOTYPES = {
                                      c_ptr,
                                      c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr]),
     "rg_launch_count": (c_i64, []),
+    "rg_count_launches": (None, [c_i64]),
     "rg_profile_enable": (None, [c_i32]),
     "rg_profile_count": (c_i32, []),
     "rg_profile_record": (ctypes.c_int, [c_i32, ctypes.c_char_p, c_i32, ctypes.POINTER(c_dbl),

@@ -37,6 +37,34 @@ from .sparse_core import ShapeError
 JOINT_PROJECTION = True
 
 
+# steps of factorizations with at most this many rows are replayed from a
+# captured CUDA graph (one per block-step index) when the caller provides a
+# StepWorkspace: at these sizes a step is launch- and sync-bound
+GRAPH_MAX_ROWS = 1 << 18
+
+
+class StepWorkspace:
+    """Device buffers of the factorizations of one solve, reused from cycle
+    to cycle, and the CUDA graphs of their steps.
+
+    A solve creates one and passes it to every ``start``; the factorization
+    of cycle c+1 then lives in the buffers of cycle c (the solver is done
+    with cycle c's basis when it starts the next), so the pointers a captured
+    step graph holds stay valid.  Each step shape is run eagerly once, then
+    captured on its second use and replayed from then on."""
+
+    def __init__(self, graphs: bool = True):
+        self._bufs = {}
+        self.graphs = {} if graphs else None
+        self._seen = set()
+
+    def buffers(self, key, make):
+        b = self._bufs.get(key)
+        if b is None:
+            b = self._bufs[key] = make()
+        return b
+
+
 class ZeroStartBlock(ValueError):
     """The starting block is numerically zero (already converged)."""
 
@@ -52,7 +80,7 @@ class ArnoldiFactorization:
     """
 
     def __init__(self, n: int, L: int, m_max: int, k: int, rank_tol: float, seed: int, device=None,
-                 dtype=torch.float64):
+                 dtype=torch.float64, workspace: StepWorkspace | None = None):
         self.n = n
         self.dtype = dtype
         npdt = np.complex128 if dtype == torch.complex128 else np.float64
@@ -63,9 +91,20 @@ class ArnoldiFactorization:
         self.m = 0
         dev = _dev.require_cuda(device)
         self.device = dev
-        # [C | W] in one allocation: C (copied in by start) directly precedes the
-        # basis, so the CGS2 projection can treat [C W] as one basis
-        self._CW = _dev.empty_block(n, k + (m_max + 1) * L, dev, dtype)
+        self._ws = workspace
+
+        def make():
+            wmax = (m_max + 1) * L
+            coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=dtype, device=dev)
+            # [C | W] in one allocation: C (copied in by start) directly precedes
+            # the basis, so the CGS2 projection can treat [C W] as one basis
+            return dict(CW=_dev.empty_block(n, k + wmax, dev, dtype), ahat=_dev.empty_block(n, L, dev, dtype),
+                        coef=coef, coef_host=torch.zeros_like(coef, device="cpu").pin_memory(),
+                        qr=QrScratch(L, dev, dtype), qr_host=torch.zeros(5 * L * L, dtype=dtype).pin_memory(),
+                        st_host=torch.zeros(2, dtype=torch.int32).pin_memory())
+
+        bufs = make() if workspace is None else workspace.buffers((n, L, m_max, k, dtype, dev), make)
+        self._CW = bufs["CW"]
         self._W = self._CW[:, k:]
         self._c_src = None  # the recycle space C copied into _CW[:, :k] (identity check in step)
         # the caller certified that R0 (hence V_1, and every later block by
@@ -76,14 +115,14 @@ class ArnoldiFactorization:
         self.z_bar = np.zeros((L, L), dtype=npdt)
         self.breakdown_events: list[str] = []
         self._rng = np.random.default_rng(seed)
-        self._ahat = _dev.empty_block(n, L, dev, dtype)
-        # packed small coefficients of one step: S1 | c1 | S2 | c2 (column-major blocks)
-        wmax = (m_max + 1) * L
-        self._coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=dtype, device=dev)
-        self._coef_host = torch.zeros_like(self._coef, device="cpu").pin_memory()
-        self._qr = QrScratch(L, dev, dtype)
-        self._qr_host = torch.zeros(5 * L * L, dtype=dtype).pin_memory()
-        self._st_host = torch.zeros(2, dtype=torch.int32).pin_memory()
+        self._ahat = bufs["ahat"]
+        # packed small coefficients of one step: S1 | c1 | S2 | c2 (column-major
+        # blocks), or G1 | G2 for the joint schedule
+        self._coef = bufs["coef"]
+        self._coef_host = bufs["coef_host"]
+        self._qr = bufs["qr"]
+        self._qr_host = bufs["qr_host"]
+        self._st_host = bufs["st_host"]
         self.launches = 0  # rg_* kernel launches issued by start/step (diagnostics)
 
     # ---- views (arnoldi.py:47-76)
@@ -194,7 +233,7 @@ def _apply_operator(opA, Z: torch.Tensor, out: torch.Tensor):
 
 
 def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: int = 0,
-          device=None, c_orthogonal: bool = False) -> ArnoldiFactorization:
+          device=None, c_orthogonal: bool = False, workspace: StepWorkspace | None = None) -> ArnoldiFactorization:
     """Initialise from the starting block R0 (arnoldi.py:98-136): V_1, z_bar
     from its thin QR; rank-deficient columns replaced by seeded random
     directions (C- and V_1-orthogonalised twice) and logged.
@@ -202,7 +241,9 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     ``c_orthogonal`` (keyword, not in the reference): the caller certifies
     that R0 was already projected against the recycle space C (the solver
     scrubs it, solver.py:149-155).  Only then may ``step`` project against
-    [C W] as one basis; the default keeps the reference's C-then-W order."""
+    [C W] as one basis; the default keeps the reference's C-then-W order.
+    ``workspace`` (keyword, not in the reference): a StepWorkspace whose
+    buffers (and captured step graphs) the factorization reuses."""
     dev = _dev.require_cuda(device if device is not None else
                             (R0.device if isinstance(R0, torch.Tensor) and R0.is_cuda else None))
     R0d = _as_block_on(R0, dev)
@@ -215,7 +256,7 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     k = recycle.k if recycle is not None else 0
     if recycle is not None and recycle.c_device().dtype != R0d.dtype:
         R0d = R0d.to(recycle.c_device().dtype) if R0d.dtype == torch.float64 else R0d
-    fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev, R0d.dtype)
+    fact = ArnoldiFactorization(n, L, m_max, k, rank_tol, seed, dev, R0d.dtype, workspace=workspace)
     if recycle is not None and k:
         fact._CW[:, :k].copy_(recycle.c_device())
         fact._c_src = recycle.c_device()
@@ -239,15 +280,26 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     return fact
 
 
-def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False):
-    """Thin QR X -> Q (Q must not alias X).  Returns (R, flagged)."""
+def _qr_enqueue(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False) -> bool:
+    """Enqueue CholQR2 of X into Q and the D2H copies of its small results
+    (no host sync).  False when the block is too wide for one CholQR2 launch
+    (``_qr_collect`` then runs the TSQR / panelled path)."""
+    if X.shape[1] > _dev.max_p(X):
+        return False
+    scr = fact._qr
+    cholqr2_launch(X, Q, scr, g1_ready=g1_ready)
+    fact._qr_host.copy_(scr.buf, non_blocking=True)
+    fact._st_host.copy_(scr.status, non_blocking=True)
+    return True
+
+
+def _qr_collect(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, enqueued: bool):
+    """After the stream has synchronised: (R, flagged) of the CholQR2, or the
+    Householder TSQR fallback when CholQR2 was not attempted or failed its
+    conditioning check (dense_kernels.py:31-48 semantics either way)."""
     L = X.shape[1]
     scr = fact._qr
-    if L <= _dev.max_p(X):
-        cholqr2_launch(X, Q, scr, g1_ready=g1_ready)
-        fact._qr_host.copy_(scr.buf, non_blocking=True)
-        fact._st_host.copy_(scr.status, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+    if enqueued:
         ok, R, norm_x = cholqr2_finish(fact._qr_host.numpy(), fact._st_host.numpy(), L)
         if ok:
             return R, _flags(R, norm_x, fact.rank_tol)
@@ -264,31 +316,43 @@ def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_r
     return R, _flags(R, norm_x, fact.rank_tol)
 
 
-def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> ArnoldiFactorization:
-    """Advance by one block step (arnoldi.py:139-193)."""
-    if fact.m >= fact.m_max:
-        raise ValueError(f"factorization at capacity m_max={fact.m_max}")
-    if ortho not in ("mgs", "cgs2"):
-        raise ValueError(f"unknown orthogonalization '{ortho}'")
-    m, L = fact.m, fact.L
-    cols = slice(m * L, (m + 1) * L)
-    Vm = fact.v_block(m)
-    Ahat = fact._ahat
-    _apply_operator(opA, Vm, Ahat)
-    C = recycle.c_device() if recycle is not None else None
+def _block_qr(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False):
+    """Thin QR X -> Q (Q must not alias X).  Returns (R, flagged)."""
+    enq = _qr_enqueue(fact, X, Q, g1_ready)
+    torch.cuda.current_stream().synchronize()
+    return _qr_collect(fact, X, Q, enq)
+
+
+def _capturable(opA):
+    """The solver's operator object behind ``opA`` when its application is
+    pure device work that a CUDA graph can hold (a CsrMatrix, no
+    preconditioner -- the ILU wave solves carry a per-call epoch -- and no
+    row partition), else None."""
+    owner = getattr(opA, "__self__", None)
+    if owner is None or getattr(opA, "__name__", "") != "apply":
+        return None
+    if getattr(owner, "_csr", None) is None or getattr(owner, "precond", None) is not None:
+        return None
+    return owner
+
+
+def _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, count=True):
+    """The device work of one CGS2 step up to the QR: A V_m, the projection,
+    the coefficient D2H and the CholQR2 (+ its D2H).  Returns whether the QR
+    was enqueued."""
+    L = fact.L
+    Vm, Ahat, Vnew = fact.v_block(m), fact._ahat, fact.v_block(m + 1)
+    if owner is not None and not count:
+        owner._base_into(Vm, Ahat)  # graph capture: each replay accounts its matvecs
+    else:
+        _apply_operator(opA, Vm, Ahat)
     active = fact._W[:, : (m + 1) * L]
     scr = fact._qr
-    Vnew = fact.v_block(m + 1)
-
     k_, w_ = fact.k, (m + 1) * L
-    # [C W] as one basis when the caller certified C-orthogonality at start
-    # and C is the recycle space copied in front of W (real data; the complex
-    # tall pass has no aliased-term merge): 3 passes instead of 5
-    joint = (JOINT_PROJECTION and ortho == "cgs2" and C is not None and k_ > 0 and fact.c_orthogonal
-             and fact._c_src is C and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
-    if ortho == "cgs2" and joint:
+    g1 = L <= _dev.max_p(Ahat)
+    if joint:
         CW = fact._CW[:, : k_ + w_]
-        if _dev.fused_ok() and L <= _dev.MAX_P_FUSED:
+        if fused:
             # rg_cgs2_f64 runs the same three passes on the adjacent [C W]
             _dev.cgs2(Ahat, fact._CW[:, :k_], active, fact._coef, scr.G1, joint=True)
         else:
@@ -297,22 +361,10 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
             G2 = fact._coef[kw * L: 2 * kw * L].view(L, kw).t()
             _dev.tall(Ahat, None, gram=("basis", CW, G1))
             _dev.tall(Ahat, None, [(CW, G1, -1.0)], gram=("basis", CW, G2))
-            _dev.tall(Ahat, Ahat, [(CW, G1, -1.0), (CW, G2, -1.0)],
-                      gram=("self", scr.G1) if L <= _dev.max_p(Ahat) else None)
+            _dev.tall(Ahat, Ahat, [(CW, G1, -1.0), (CW, G2, -1.0)], gram=("self", scr.G1) if g1 else None)
         ncoef = 2 * (k_ + w_) * L
-        fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
-        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.max_p(Ahat))
-        hc = fact._coef_host.numpy()
-        kw = k_ + w_
-        hG1 = hc[: kw * L].reshape(L, kw).T
-        hG2 = hc[kw * L: 2 * kw * L].reshape(L, kw).T
-        fact._F[:, cols] += hG1[:k_]
-        fact._F[:, cols] += hG2[:k_]
-        fact._H[: (m + 1) * L, cols] += hG1[k_:]
-        fact._H[: (m + 1) * L, cols] += hG2[k_:]
-    elif ortho == "cgs2":
-        if (_dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED and fact.k <= _dev.MAX_GC
-                and (m + 1) * L <= _dev.MAX_GC):
+    else:
+        if fused:
             # one C-ABI call runs the same fused pass schedule (rg_cgs2_f64);
             # C is passed from its own allocation here, so the five-pass
             # sequential schedule applies
@@ -323,26 +375,92 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
                 bases, coefs = [C, active, C, active], [S1, c1, S2, c2]
             else:
                 bases, coefs = [active, active], [c1, c2]
-            project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if L <= _dev.max_p(Ahat) else None)
+            project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if g1 else None)
         ncoef = (2 * fact.k + 2 * (m + 1) * L) * L
-        fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
-        R, flagged = _block_qr(fact, Ahat, Vnew, g1_ready=L <= _dev.max_p(Ahat))
-        hc = fact._coef_host.numpy()
-        k, w = fact.k, (m + 1) * L
-        off = 0
-        blocks = []
-        for rows in (k, w, k, w):
-            blocks.append(hc[off: off + rows * L].reshape(L, rows).T)
-            off += rows * L
-        hS1, hc1, hS2, hc2 = blocks
-        if C is not None:
-            fact._F[:, cols] += hS1
-            fact._F[:, cols] += hS2
-        fact._H[: (m + 1) * L, cols] += hc1
-        fact._H[: (m + 1) * L, cols] += hc2
+    fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
+    return _qr_enqueue(fact, Ahat, Vnew, g1_ready=g1)
+
+
+def _replay_step(fact, opA, owner, C, m, joint):
+    """Graph path of one step: the device work of ``_cgs2_enqueue`` captured
+    once per (step index, schedule, operator, C) and replayed.  Returns
+    whether the QR was enqueued, or None when this shape runs eagerly."""
+    ws = fact._ws
+    key = (m, joint, id(owner), 0 if (joint or C is None) else C.data_ptr())
+    hit = ws.graphs.get(key)
+    if hit is None:
+        if key not in ws._seen:  # first use: eager (warms every launch path and buffer)
+            ws._seen.add(key)
+            return None
+        g = torch.cuda.CUDAGraph()
+        lib = _dev.lib()
+        before = lib.rg_launch_count()
+        torch.cuda.current_stream().synchronize()
+        with torch.cuda.graph(g):
+            enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, True, count=False)
+        hit = ws.graphs[key] = (g, enq, int(lib.rg_launch_count() - before))
+    g, enq, nlaunch = hit
+    g.replay()
+    owner.count += fact.L
+    _dev.lib().rg_count_launches(nlaunch)
+    return enq
+
+
+def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> ArnoldiFactorization:
+    """Advance by one block step (arnoldi.py:139-193)."""
+    if fact.m >= fact.m_max:
+        raise ValueError(f"factorization at capacity m_max={fact.m_max}")
+    if ortho not in ("mgs", "cgs2"):
+        raise ValueError(f"unknown orthogonalization '{ortho}'")
+    m, L = fact.m, fact.L
+    cols = slice(m * L, (m + 1) * L)
+    C = recycle.c_device() if recycle is not None else None
+    active = fact._W[:, : (m + 1) * L]
+    Vnew = fact.v_block(m + 1)
+    k_, w_ = fact.k, (m + 1) * L
+
+    if ortho == "mgs":
+        _apply_operator(opA, fact.v_block(m), fact._ahat)
+        _mgs_project(fact, fact._ahat, C, m, cols)
+        R, flagged = _block_qr(fact, fact._ahat, Vnew)
     else:
-        _mgs_project(fact, Ahat, C, m, cols)
-        R, flagged = _block_qr(fact, Ahat, Vnew)
+        # [C W] as one basis when the caller certified C-orthogonality at start
+        # and C is the recycle space copied in front of W (real data; the
+        # complex tall pass has no aliased-term merge): 3 passes instead of 5
+        joint = (JOINT_PROJECTION and C is not None and k_ > 0 and fact.c_orthogonal and fact._c_src is C
+                 and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
+        fused = (_dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED
+                 and (joint or (k_ <= _dev.MAX_GC and w_ <= _dev.MAX_GC)))
+        enq = None
+        owner = _capturable(opA)
+        if (fused and owner is not None and fact._ws is not None and fact._ws.graphs is not None
+                and fact.n <= GRAPH_MAX_ROWS and not _dev.LaunchLog.timing):
+            enq = _replay_step(fact, opA, owner, C, m, joint)
+        if enq is None:
+            enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, fused)
+        torch.cuda.current_stream().synchronize()  # the step's one host sync
+        R, flagged = _qr_collect(fact, fact._ahat, Vnew, enq)
+        hc = fact._coef_host.numpy()
+        if joint:
+            kw = k_ + w_
+            hG1 = hc[: kw * L].reshape(L, kw).T
+            hG2 = hc[kw * L: 2 * kw * L].reshape(L, kw).T
+            fact._F[:, cols] += hG1[:k_]
+            fact._F[:, cols] += hG2[:k_]
+            fact._H[: (m + 1) * L, cols] += hG1[k_:]
+            fact._H[: (m + 1) * L, cols] += hG2[k_:]
+        else:
+            off = 0
+            blocks = []
+            for rows in (k_, w_, k_, w_):
+                blocks.append(hc[off: off + rows * L].reshape(L, rows).T)
+                off += rows * L
+            hS1, hc1, hS2, hc2 = blocks
+            if C is not None:
+                fact._F[:, cols] += hS1
+                fact._F[:, cols] += hS2
+            fact._H[: (m + 1) * L, cols] += hc1
+            fact._H[: (m + 1) * L, cols] += hc2
 
     fact._H[(m + 1) * L: (m + 2) * L, cols] = R
     for j in np.flatnonzero(flagged):

@@ -109,6 +109,8 @@ extern "C" void rg_profile_enable(int32_t on) {
 
 extern "C" int64_t rg_launch_count(void) { return rg::g_launches.load(); }
 
+extern "C" void rg_count_launches(int64_t n) { rg::g_launches += n; }
+
 extern "C" int32_t rg_profile_count(void) {
   std::lock_guard<std::mutex> lk(rg::g_mu);
   return (int32_t)rg::g_recs.size();

@@ -27,7 +27,7 @@ def _run_case(g, name, ortho, c_orthogonal=False):
     return A, fact, k
 
 
-def _check_against_golden(test, g, name, A, fact, k, h_tol=1e-12, w_tol=1e-10):
+def _check_against_golden(test, g, name, A, fact, k, h_tol=1e-12, w_tol=1e-12):
     scale = A.frobenius_norm()
     eh = np.abs(fact.h_bar - g[f"{name}/H"]).max() / scale
     ez = np.abs(fact.z_bar - g[f"{name}/z_bar"]).max() / np.abs(g[f"{name}/z_bar"]).max()
@@ -72,7 +72,7 @@ def test_bases_wider_than_one_gram_launch(cuda, name):
     pass chain instead of failing."""
     g = load_golden("r2_cases.npz")
     A, fact, k = _run_case(g, name, "cgs2", c_orthogonal=True)
-    _check_against_golden("wide", g, name, A, fact, k, h_tol=1e-11)
+    _check_against_golden("wide", g, name, A, fact, k)
 
 
 def test_wide_cycle_solve_matches_reference(cuda):
@@ -114,3 +114,29 @@ def test_reference_rgmrecyc_file_loads_to_device(cuda, tmp_path):
     assert np.array_equal(u, g["rgmrecyc/u"]) and np.array_equal(c, g["rgmrecyc/c"])
     save_recycle_space(rs, tmp_path / "again.rgm")
     assert (tmp_path / "again.rgm").read_bytes() == ref_bytes
+
+
+def test_graph_replayed_steps_are_bitwise_the_eager_steps(cuda):
+    """Config 1 (n = 4096) runs its block steps from captured CUDA graphs
+    (arnoldi.StepWorkspace); the replayed kernels see the same operands, so
+    the whole sequence is bitwise the eager one -- and still the reference's
+    (test_gpu_solver.test_cfg1_sequence_matches_reference runs with graphs)."""
+    from paper_1604_01713_b200 import SolverConfig, arnoldi, problems, solve_sequence
+    from paper_1604_01713_b200 import device as D
+
+    systems, kw = problems.cfg1_sequence()
+    runs = {}
+    for graphs in (False, True):
+        old = arnoldi.GRAPH_MAX_ROWS
+        arnoldi.GRAPH_MAX_ROWS = (1 << 18) if graphs else 0
+        try:
+            before = D.lib().rg_launch_count()
+            runs[graphs] = (solve_sequence(systems, SolverConfig(**kw)), D.lib().rg_launch_count() - before)
+        finally:
+            arnoldi.GRAPH_MAX_ROWS = old
+    (eager, n_eager), (graph, n_graph) = runs[False], runs[True]
+    for a, b in zip(eager, graph):
+        assert a.cycles == b.cycles and a.matvec_count == b.matvec_count
+        assert np.array_equal(np.concatenate(a.residual_history), np.concatenate(b.residual_history))
+        assert np.array_equal(a.solution, b.solution)
+    assert n_graph == n_eager  # replays report the kernels they run
