@@ -39,8 +39,14 @@ JOINT_PROJECTION = True
 
 # steps of factorizations with at most this many rows are replayed from a
 # captured CUDA graph (one per block-step index) when the caller provides a
-# StepWorkspace: at these sizes a step is launch- and sync-bound
+# StepWorkspace with graphs on: at these sizes a step is launch- and
+# sync-bound.  Measured on B200 for config 1 (n = 4096, tools/prof_cfg1_step.py,
+# profiles/cfg1_graph_r02.json): a replayed step takes 0.147 ms against 0.195
+# ms eager, but one solve uses each (step index, k) shape only a few times, so
+# capture + instantiation outweigh the saving (3-system sequence 0.267 s with
+# graphs vs 0.250 s eager) -- hence off by default (STEP_GRAPHS).
 GRAPH_MAX_ROWS = 1 << 18
+STEP_GRAPHS = False
 
 
 class StepWorkspace:
@@ -50,13 +56,18 @@ class StepWorkspace:
     A solve creates one and passes it to every ``start``; the factorization
     of cycle c+1 then lives in the buffers of cycle c (the solver is done
     with cycle c's basis when it starts the next), so the pointers a captured
-    step graph holds stay valid.  Each step shape is run eagerly once, then
-    captured on its second use and replayed from then on."""
+    step graph holds stay valid.  Each step shape runs eagerly
+    ``capture_after`` times, is then captured, and replayed from then on
+    (capture + instantiation cost a few eager steps, so shapes used only a
+    couple of times per solve never pay for a graph)."""
 
-    def __init__(self, graphs: bool = True):
+    def __init__(self, graphs: bool | None = None, capture_after: int = 1):
         self._bufs = {}
-        self.graphs = {} if graphs else None
-        self._seen = set()
+        self.graphs = {} if (STEP_GRAPHS if graphs is None else graphs) else None
+        self._seen = {}
+        self.capture_after = capture_after  # eager runs of a step shape before it is captured
+        self.scratch = None  # the captured steps' own rg_tall workspace
+        self.stream = None   # capture stream
 
     def buffers(self, key, make):
         b = self._bufs.get(key)
@@ -383,22 +394,40 @@ def _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, count=True):
 
 def _replay_step(fact, opA, owner, C, m, joint):
     """Graph path of one step: the device work of ``_cgs2_enqueue`` captured
-    once per (step index, schedule, operator, C) and replayed.  Returns
+    once per (step index, schedule, operator, buffers, C) and replayed.  Returns
     whether the QR was enqueued, or None when this shape runs eagerly."""
     ws = fact._ws
-    key = (m, joint, id(owner), 0 if (joint or C is None) else C.data_ptr())
+    # the factorization's buffers differ per (k, L, ...) shape: key on them too
+    key = (m, joint, id(owner), fact._CW.data_ptr(), fact.k, 0 if (joint or C is None) else C.data_ptr())
     hit = ws.graphs.get(key)
     if hit is None:
-        if key not in ws._seen:  # first use: eager (warms every launch path and buffer)
-            ws._seen.add(key)
+        seen = ws._seen.get(key, 0)
+        if seen < ws.capture_after:  # eager first (warms every launch path and buffer)
+            ws._seen[key] = seen + 1
             return None
         g = torch.cuda.CUDAGraph()
         lib = _dev.lib()
+        if ws.scratch is None:
+            # every Gram of the step: <= 128 basis columns per launch, <= 256
+            # requested by the sequential orchestrator call
+            ws.scratch = torch.zeros(lib.rg_tall_workspace_bytes(fact.n, max(fact.L, 16), 0, 0, 1, 256),
+                                     dtype=torch.uint8, device=fact.device)
+        if ws.stream is None:
+            ws.stream = torch.cuda.Stream(fact.device)
         before = lib.rg_launch_count()
-        torch.cuda.current_stream().synchronize()
-        with torch.cuda.graph(g):
-            enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, True, count=False)
-        hit = ws.graphs[key] = (g, enq, int(lib.rg_launch_count() - before))
+        # capture on a side stream with the low-level API (torch.cuda.graph's
+        # context manager also runs gc.collect() and empty_cache() per capture)
+        ws.stream.wait_stream(torch.cuda.current_stream())
+        with _dev.Workspace.fixed(ws.scratch), torch.cuda.stream(ws.stream):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, True, count=False)
+            finally:
+                g.capture_end()
+        torch.cuda.current_stream().wait_stream(ws.stream)
+        nl = int(lib.rg_launch_count() - before)
+        lib.rg_count_launches(-nl)  # captured, not run: each replay reports its kernels
+        hit = ws.graphs[key] = (g, enq, nl)
     g, enq, nlaunch = hit
     g.replay()
     owner.count += fact.L

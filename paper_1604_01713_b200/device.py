@@ -10,8 +10,8 @@ torch is used only as the allocator / stream provider.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
-
 import os
 
 import numpy as np
@@ -184,6 +184,19 @@ class Workspace:
     _pools: dict = {}
     _guard = int(os.environ.get("RG_WS_GUARD", "0"))
     _last = None
+    _override = None  # fixed slot-0 buffer while a CUDA graph is captured (see ``fixed``)
+
+    @classmethod
+    @contextlib.contextmanager
+    def fixed(cls, buf: torch.Tensor):
+        """Serve every slot-0 request from ``buf`` inside the block: a captured
+        CUDA graph keeps the pointers it saw, so its workspace must not be the
+        pool buffer that later, larger requests replace."""
+        prev, cls._override = cls._override, buf
+        try:
+            yield
+        finally:
+            cls._override = prev
 
     @classmethod
     def check(cls, label: str) -> None:
@@ -198,6 +211,10 @@ class Workspace:
     @classmethod
     def get(cls, nbytes: int, device=None, slot: int = 0) -> torch.Tensor:
         dev = require_cuda(device)
+        if cls._override is not None and slot == 0:
+            if cls._override.numel() < nbytes:
+                raise RuntimeError(f"fixed workspace of {cls._override.numel()} bytes < {nbytes} requested")
+            return cls._override
         if cls._guard:
             nb = max(int(nbytes), 256)
             buf = torch.zeros(nb + cls._guard, dtype=torch.uint8, device=dev)

@@ -117,23 +117,23 @@ def test_reference_rgmrecyc_file_loads_to_device(cuda, tmp_path):
 
 
 def test_graph_replayed_steps_are_bitwise_the_eager_steps(cuda):
-    """Config 1 (n = 4096) runs its block steps from captured CUDA graphs
-    (arnoldi.StepWorkspace); the replayed kernels see the same operands, so
-    the whole sequence is bitwise the eager one -- and still the reference's
-    (test_gpu_solver.test_cfg1_sequence_matches_reference runs with graphs)."""
+    """Config 1 (n = 4096) with its block steps replayed from captured CUDA
+    graphs (arnoldi.STEP_GRAPHS, arnoldi.StepWorkspace): the replayed kernels
+    see the same operands, so the whole sequence is bitwise the eager one
+    (which test_gpu_solver pins to the reference), with the same kernel count."""
     from paper_1604_01713_b200 import SolverConfig, arnoldi, problems, solve_sequence
     from paper_1604_01713_b200 import device as D
 
     systems, kw = problems.cfg1_sequence()
     runs = {}
     for graphs in (False, True):
-        old = arnoldi.GRAPH_MAX_ROWS
-        arnoldi.GRAPH_MAX_ROWS = (1 << 18) if graphs else 0
+        old = arnoldi.STEP_GRAPHS
+        arnoldi.STEP_GRAPHS = graphs
         try:
             before = D.lib().rg_launch_count()
             runs[graphs] = (solve_sequence(systems, SolverConfig(**kw)), D.lib().rg_launch_count() - before)
         finally:
-            arnoldi.GRAPH_MAX_ROWS = old
+            arnoldi.STEP_GRAPHS = old
     (eager, n_eager), (graph, n_graph) = runs[False], runs[True]
     for a, b in zip(eager, graph):
         assert a.cycles == b.cycles and a.matvec_count == b.matvec_count

@@ -17,8 +17,13 @@ import torch  # noqa: E402
 from paper_1604_01713_b200 import SolverConfig, arnoldi, problems, solve_sequence  # noqa: E402
 
 
-def run(graphs: bool, reps: int = 3):
-    arnoldi.GRAPH_MAX_ROWS = (1 << 18) if graphs else 0
+def run(graphs: bool, reps: int = 3, after: int = 2):
+    orig_ws = arnoldi.StepWorkspace.__init__
+
+    def ws_init(self, graphs_=None, capture_after=after):
+        orig_ws(self, graphs, capture_after)
+
+    arnoldi.StepWorkspace.__init__ = ws_init
     systems, kw = problems.cfg1_sequence()
     step_t = []
     orig = arnoldi.step
@@ -41,8 +46,9 @@ def run(graphs: bool, reps: int = 3):
             walls.append(time.perf_counter() - t0)
     finally:
         arnoldi.step = orig
+        arnoldi.StepWorkspace.__init__ = orig_ws
     steps = [int(sum(len(h) for h in r.residual_history)) for r in reps_]
-    return {"graphs": graphs, "sequence_s": min(walls), "steps": steps,
+    return {"graphs": graphs, "capture_after": after, "sequence_s": min(walls), "steps": steps,
             "step_ms_median": 1e3 * float(np.median(step_t)), "step_ms_mean": 1e3 * float(np.mean(step_t)),
             "hist": [np.concatenate(r.residual_history).tolist() for r in reps_]}
 
@@ -50,8 +56,8 @@ def run(graphs: bool, reps: int = 3):
 if __name__ == "__main__":
     torch.cuda.set_device(0)
     off = run(False)
-    on = run(True)
-    same = off["hist"] == on["hist"]
-    for r in (off, on):
+    ons = [run(True, after=a) for a in (1, 2, 3, 5)]
+    same = all(off["hist"] == on["hist"] for on in ons)
+    for r in [off] + ons:
         r.pop("hist")
-    print(json.dumps({"cfg1_step_graphs": on, "cfg1_step_eager": off, "identical_histories": same}))
+    print(json.dumps({"cfg1_step_eager": off, "cfg1_step_graphs": ons, "identical_histories": same}))
