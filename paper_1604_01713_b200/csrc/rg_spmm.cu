@@ -21,6 +21,14 @@
 
 #include <cstdlib>
 
+// A/B build switch (tools/ab_build.py): RG_SPMM_COLS=0 keeps single-column
+// blocks on the entry-outer loop.  (A row-major X, one 64-byte gather per
+// entry at p = 8, measured 1185 vs 819 us at cfg4 -- tools/ab_spmm.py,
+// profiles/spmm_r02.txt -- and was dropped.)
+#ifndef RG_SPMM_COLS
+#define RG_SPMM_COLS 1
+#endif
+
 namespace rg {
 
 constexpr int kSpmmWarps = 8;     // 256 threads per CTA
@@ -100,6 +108,69 @@ __device__ __forceinline__ void accumulate_rows(const int32_t* sci, const double
   }
 }
 
+// Column-outer accumulation (single-column blocks; measured on B200, cfg4
+// 256^3 p = 1: 311 vs 374 us, tools/ab_spmm.py -- for p >= 4 it is 1.5-3x
+// slower than the entry-outer loop): a lane loads up to kSpmmU of its row's
+// staged entries (index, value) into registers once, then gathers those
+// entries' X values two columns at a time -- 2*kSpmmU independent loads in
+// flight per lane instead of one entry's PB -- and adds them in storage
+// order.  Per (row, column) the operation sequence is still the reference's
+// (t ascending, separately rounded product and sum), so the output is
+// bitwise the same.
+constexpr int kSpmmU = 8;
+
+template <int PB, bool GHOST>
+__device__ __forceinline__ void accumulate_cols(const int32_t* sci, const double* sva, int lo, int hi,
+                                                const double* __restrict__ X, int64_t ldx, int64_t n_local,
+                                                const double* __restrict__ Xg, int64_t ldg, double (&acc)[PB]) {
+  for (int t0 = lo; t0 < hi; t0 += kSpmmU) {
+    const int cnt = min(kSpmmU, hi - t0);
+    int32_t j[kSpmmU];
+#pragma unroll
+    for (int u = 0; u < kSpmmU; ++u) j[u] = u < cnt ? sci[t0 + u] : 0;
+    const double* a = sva + t0;  // values re-read from shared memory per column pair
+#pragma unroll
+    for (int c = 0; c < PB; c += 2) {
+      double x0[kSpmmU], x1[kSpmmU];
+      const double* X0 = X + (int64_t)c * ldx;
+      const double* X1 = X0 + ldx;
+#pragma unroll
+      for (int u = 0; u < kSpmmU; ++u) {
+        if (u < cnt) {
+          if (GHOST && j[u] >= n_local) {
+            const double* g = Xg + (j[u] - n_local) + (int64_t)c * ldg;
+            x0[u] = __ldg(g);
+            if (c + 1 < PB) x1[u] = __ldg(g + ldg);
+          } else {
+            x0[u] = __ldg(X0 + j[u]);
+            if (c + 1 < PB) x1[u] = __ldg(X1 + j[u]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSpmmU; ++u) {
+        if (u < cnt) {
+          acc[c] = __dadd_rn(acc[c], __dmul_rn(a[u], x0[u]));
+          if (c + 1 < PB) acc[c + 1] = __dadd_rn(acc[c + 1], __dmul_rn(a[u], x1[u]));
+        }
+      }
+      // keep the next column pair's gathers behind this one (the compiler
+      // would otherwise hoist all PB*kSpmmU loads and spill)
+      asm volatile("" ::: "memory");
+    }
+  }
+}
+
+template <int PB, bool GHOST>
+__device__ __forceinline__ void accumulate_unit(const int32_t* sci, const double* sva, int lo, int hi,
+                                                const double* __restrict__ X, int64_t ldx, int64_t n_local,
+                                                const double* __restrict__ Xg, int64_t ldg, double (&acc)[PB]) {
+  if (RG_SPMM_COLS && PB == 1)
+    accumulate_cols<PB, GHOST>(sci, sva, lo, hi, X, ldx, n_local, Xg, ldg, acc);
+  else
+    accumulate_rows<PB, GHOST>(sci, sva, lo, hi, X, ldx, n_local, Xg, ldg, acc);
+}
+
 // CTAs per SM the register budget is sized for: 3 (85 registers) spills at
 // PB >= 6, and the spill traffic costs more than the extra warps buy
 // (cfg4 p = 8: 912 us with 3, 824 us with 2; profiles/spmm_r01.txt)
@@ -161,7 +232,7 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
     for (int c = 0; c < PB; ++c) acc[c] = 0.0;
     const int32_t cnt = cur.wend - cur.wbeg;
     if (cnt <= CH) {
-      accumulate_rows<PB, GHOST>(s_ci[w][buf], s_va[w][buf], cur.mybeg - cur.wbeg, cur.myend - cur.wbeg, X, ldx,
+      accumulate_unit<PB, GHOST>(s_ci[w][buf], s_va[w][buf], cur.mybeg - cur.wbeg, cur.myend - cur.wbeg, X, ldx,
                                  n_local, Xg, ldg, acc);
     } else {
       // long rows: chunked synchronous staging through this unit's buffer
@@ -177,7 +248,7 @@ spmm_persist_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restric
         __syncwarp();
         const int lo = max(cur.mybeg, base) - base;
         const int hi = min(cur.myend, base + c2) - base;
-        accumulate_rows<PB, GHOST>(sci, sva, lo, hi, X, ldx, n_local, Xg, ldg, acc);
+        accumulate_unit<PB, GHOST>(sci, sva, lo, hi, X, ldx, n_local, Xg, ldg, acc);
       }
     }
     if (i < row_end) {

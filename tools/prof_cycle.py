@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=128)
     ap.add_argument("--systems", type=int, default=2)
+    ap.add_argument("--kernels", action="store_true", help="also attribute device time per kernel label")
     args = ap.parse_args()
     from paper_1604_01713_b200 import SolverConfig, arnoldi, dense_kernels, problems, recycling, solver
 
@@ -56,6 +57,10 @@ def main():
     solver.solve_block_gcrodr(system(0), B[:, :], None, SolverConfig(m=2, k=4, max_cycles=1))  # warm-up
     acc.clear()
     cnt.clear()
+    from paper_1604_01713_b200 import device as D
+
+    if args.kernels:
+        D.LaunchLog.reset(timing=True)
     rs = None
     t0 = time.perf_counter()
     steps = 0
@@ -68,6 +73,12 @@ def main():
     out = {"grid": args.grid, "total_s": total, "cycles": cycles, "block_steps": steps,
            "phases_s": {k: round(v, 4) for k, v in sorted(acc.items(), key=lambda kv: -kv[1])},
            "calls": dict(cnt)}
+    if args.kernels:
+        summ = D.LaunchLog.summary()
+        D.LaunchLog.reset(timing=False)
+        out["kernels"] = {k: {"calls": v[0], "ms": round(v[1], 2), "GB/s": round(v[2] / max(v[1], 1e-9) / 1e6, 1)}
+                          for k, v in sorted(summ.items(), key=lambda kv: -kv[1][1])}
+        out["kernel_ms_total"] = round(sum(v[1] for v in summ.values()), 1)
     print(json.dumps(out, indent=1))
 
 
