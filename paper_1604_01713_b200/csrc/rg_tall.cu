@@ -34,8 +34,11 @@
 // the FP64 tensor path on sm_100a.
 #include "rg_common.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 namespace rg {
 
@@ -1094,11 +1097,29 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
 //   store    Zout rows                 (optional)
 //   Gram     G += Gb^T z  or  z^T z    (DMMA; Gb may alias X: P2 of the
 //                                       joint schedule reads X once)
-// and release the stage with one mbarrier arrive per warp.  Column stride
-// 72 doubles (== 8 mod 16): the scalar update fragments and the 16-byte Gram
-// fragments (k mapped to row pairs) are bank-conflict free.  (A first cut
-// with one cp.async.bulk per column segment ran at 2.4 TB/s: ~50 cycles per
-// 512-byte bulk copy per SM.)
+// and release the stage with one mbarrier arrive per warp.
+//
+// Two ways to fill a stage (template flag TMA):
+//   TMA   (default) one elected producer thread issues ONE
+//         cp.async.bulk.tensor.2d per operand per stage -- a box of 72 rows x
+//         up to 128 columns (64 KB) -- with mbarrier complete_tx.  The box
+//         lands densely as [column][72 rows]; a column stride of 72 doubles
+//         (== 8 mod 16) keeps both fragment orders conflict free.  Stages
+//         advance by 64 rows (8 consumer warps, 2 per SMSP -- a 9th warp
+//         unbalances the DMMA-heavy passes), so consecutive boxes overlap by
+//         8 rows that are only padding: +12.5% L2->SM bytes, no extra DRAM
+//         bytes (the neighbouring CTA fetches those rows at the same time).
+//         Rows past n and columns past the operand width arrive as zeros
+//         (out-of-bounds fill).
+//   else  (fallback: an operand the tensor map cannot describe) 2 producer
+//         warps issue 16-byte cp.async per lane into the same 72-stride
+//         layout, each lane's completion counted on the stage's mbarrier.
+// Measured TMA streaming rate per box shape (tools/tma_bw.cu,
+// profiles/tma_r02.txt): the tensor engine spends ~8 cycles per box row,
+// so boxes with 64-byte rows stream at 2.3 TB/s, 128-byte rows at 4.6 TB/s,
+// and >= 256-byte rows at 7.2-7.3 TB/s; hence whole 72-row columns per box
+// row.  (One 1-D cp.async.bulk per 512-byte column segment ran at 2.4 TB/s:
+// ~60 cycles per request.)
 // ============================================================================
 
 constexpr int kWsKS = 32;  // update k-steps (a1 <= 128)
@@ -1108,22 +1129,34 @@ constexpr size_t kWsSmemMax = 220 * 1024;
 #ifndef RG_WS_PROD8
 #define RG_WS_PROD8 2
 #endif
-// CW consumer warps x 8 rows per stage; column stride CW*8 + 8 doubles
-template <int CW>
+// CW consumer warps x 8 rows per stage.  Column stride == 8 mod 16 doubles
+// keeps both fragment orders bank-conflict free: cp.async pads CW*8 rows to
+// CW*8 + 8; a tensor request lands densely, so the TMA stage is CW*8 rows
+// with CW odd (9 warps, 72 rows).
+template <int CW, bool TMA = false>
 struct WsGeom {
-  static constexpr int kRows = CW * 8;
-  static constexpr int kS = kRows + 8;                 // == 8 mod 16
-  static constexpr int kProd = CW >= 6 ? RG_WS_PROD8 : 1;  // producer warps
+  static constexpr int kRows = CW * 8;                              // rows per stage
+  static constexpr int kS = kRows % 16 == 8 ? kRows : kRows + 8;  // column stride (TMA: box rows)
+  static_assert(kS % 16 == 8, "ws stage column stride must be 8 mod 16 doubles");
+  static constexpr int kProd = TMA ? 1 : (CW >= 6 ? RG_WS_PROD8 : 1);  // producer warps
   static constexpr int kThreads = (CW + kProd) * 32;
   static constexpr int kMinBlocks = CW >= 6 ? 1 : 2;
   static constexpr size_t kSmemMax = CW >= 6 ? kWsSmemMax : 110 * 1024;
-  // <= 8 warps: two per SMSP, room for the update's S fragments in registers
-  static constexpr bool kBregOk = CW + kProd <= 8;
 };
 
 struct WsPlan {
   int nslots, nload, x1slot0, gbslot0, stages, nz, a1, ngb;
+  // stage layout: segment offsets (doubles) and per-consumer-warp offsets
+  int stage_words;
+  int zoff, xoff, goff;  // operand segment offsets in a stage (doubles)
+  unsigned tx;           // TMA: bytes landing per stage
 };
+
+// the three operand tiles of a ws stage as 2-D tensor maps (TMA variant)
+struct WsMaps {
+  CUtensorMap z, x, g;
+};
+
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1162,18 +1195,34 @@ __device__ __forceinline__ void cp16_zfill(uint32_t dst, const void* src, int by
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+// one operand tile of a stage: box {rows, columns} at row row0
+__device__ __forceinline__ void tma_tile(double* dst, const CUtensorMap* m, int row0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+      ::"r"(smem_u32(dst)), "l"(m), "r"(row0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 
-template <int CW, int NT, int MT, int KSR = 0>
-__global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) tall_ws_kernel(TallParams P, WsPlan W) {
-  using G = WsGeom<CW>;
-  constexpr int kRows = G::kRows, kS = G::kS, kThreads = G::kThreads;
+template <int CW, int NT, int MT, int KSR = 0, bool TMA = false>
+__global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>::kMinBlocks))
+    tall_ws_kernel(TallParams P, WsPlan W, const __grid_constant__ WsMaps maps) {
+  using G = WsGeom<CW, TMA>;
+  constexpr int kRows = G::kRows, kThreads = G::kThreads;
+  constexpr int CS = G::kS;  // column stride of a stage
   constexpr int MTA = MT > 0 ? MT : 1;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double ws_smem[];
+  double* smem = ws_smem;
   __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
   __shared__ bool s_last;
   const int p = P.p;
   const int ks1 = (P.a1 + 3) / 4;
-  const size_t stage_words = (size_t)W.nslots * kS;
+  const size_t stage_words = (size_t)W.stage_words;
   double* stage0 = smem;
   double* sf1 = stage0 + (size_t)W.stages * stage_words;  // [ks1][NT][32]
   double* sR = sf1 + (size_t)ks1 * NT * 32;                // [NT*8][NT*8] solve factor
@@ -1181,7 +1230,9 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
   constexpr int PM8 = NT * 8;
   const bool trsm = KSR == 0 && (P.r1 || P.r2);  // the KSR variants never carry solves
 
-  for (size_t e = threadIdx.x; e < (size_t)W.stages * stage_words; e += kThreads) stage0[e] = 0.0;
+  // (TMA fills every stage word, zeros included)
+  if (!TMA)
+    for (size_t e = threadIdx.x; e < (size_t)W.stages * stage_words; e += kThreads) stage0[e] = 0.0;
   for (int e = threadIdx.x; e < ks1 * NT * 32; e += kThreads) {
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
     const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
@@ -1213,7 +1264,7 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < W.stages; ++s) {
-      mbar_init(&full[s], G::kProd * 32);
+      mbar_init(&full[s], TMA ? 1u : G::kProd * 32u);
       mbar_init(&empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1234,7 +1285,26 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
 
-  if (warp >= CW) {
+  if (TMA && warp >= CW) {
+    // ---------------- producer: one thread, one tensor request per operand
+    if (warp == CW && lane == 0) {
+      int s = 0;
+      unsigned ph = 0;
+      for (int64_t it = 0; it < my_units; ++it) {
+        if (it >= W.stages) mbar_wait(&empty[s], ph ^ 1u);
+        const int row0 = (int)(((int64_t)blockIdx.x + it * gridDim.x) * kRows);
+        double* st = stage0 + s * stage_words;
+        mbar_expect_tx(&full[s], W.tx);
+        if (W.nz) tma_tile(st + W.zoff, &maps.z, row0, &full[s]);
+        if (W.a1) tma_tile(st + W.xoff, &maps.x, row0, &full[s]);
+        if (W.ngb) tma_tile(st + W.goff, &maps.g, row0, &full[s]);
+        if (++s == W.stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= CW) {
     // ---------------- producers: lane t copies rows 2q, 2q + 1 (zero-filled
     // past n) of columns jl, jl + kStep, ... of each operand segment; the
     // source pointer and the slot offset advance by constants
@@ -1253,12 +1323,12 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
       const uint32_t dq = smem_u32(stage0 + s * stage_words) + (uint32_t)(2 * q * 8);
       auto segment = [&](const double* base, int64_t ld, int ncols, int slot0) {
         const double* src = base + (int64_t)jl * ld + off;
-        uint32_t d = dq + (uint32_t)((slot0 + jl) * kS * 8);
+        uint32_t d = dq + (uint32_t)((slot0 + jl) * G::kS * 8);
 #pragma unroll 4
         for (int j = jl; j < ncols; j += kStep) {
           cp16_zfill(d, src, bytes);
           src += kStep * ld;
-          d += kStep * kS * 8;
+          d += kStep * G::kS * 8;
         }
       };
       if (W.nz) segment(P.zin, P.ldzin, W.nz, 0);
@@ -1272,7 +1342,8 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
     }
     cp_async_wait<0>();
   } else {
-    // ---------------- consumers: warp owns stage rows rw .. rw + 7
+    // ---------------- consumers: warp owns stage rows rw .. rw + 7; element
+    // (stage row r, column c) of an operand segment is at seg[c * CS + r]
     const int mrow = lane >> 2, kq = lane & 3;
     const int rw = warp * 8;
     const bool upd = P.a1 > 0;
@@ -1293,22 +1364,22 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
       mbar_wait(&full[s], ph);
       double* st = stage0 + s * stage_words;
       const int64_t r0 = ((int64_t)blockIdx.x + it * gridDim.x) * kRows;
-      double* zs = st;  // slots 0 .. NT*8-1
+      double* zs = st + W.zoff + rw;  // this warp's z rows
       if (upd) {
         double zf[NT][2], m[kWsNacc][NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            zf[nt][v] = zs[(nt * 8 + 2 * kq + v) * kS + rw + mrow];
+            zf[nt][v] = W.nz ? zs[(nt * 8 + 2 * kq + v) * CS + mrow] : 0.0;
 #pragma unroll
             for (int q = 0; q < kWsNacc; ++q) m[q][nt][v] = 0.0;
           }
-        const double* xs = st + W.x1slot0 * kS + kq * kS + rw + mrow;
+        const double* xs = st + W.xoff + rw + kq * CS + mrow;
 #pragma unroll
         for (int ks = 0; ks < kKS; ++ks) {
           if (ks < ks1) {
-            const double a = xs[ks * 4 * kS];
+            const double a = xs[ks * 4 * CS];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
               dmma_nv(m[ks % kWsNacc][nt][0], m[ks % kWsNacc][nt][1], a,
@@ -1328,7 +1399,7 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-            for (int v = 0; v < 2; ++v) zs[(nt * 8 + 2 * kq + v) * kS + rw + mrow] = zf[nt][v];
+            for (int v = 0; v < 2; ++v) zs[(nt * 8 + 2 * kq + v) * CS + mrow] = zf[nt][v];
           __syncwarp();
         }
       }
@@ -1337,10 +1408,10 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
         if (lane < 8) {
           double zr[PM8];
 #pragma unroll
-          for (int c = 0; c < PM8; ++c) zr[c] = zs[c * kS + rw + lane];
+          for (int c = 0; c < PM8; ++c) zr[c] = zs[c * CS + lane];
           trsm_row<PM8>(zr, sR, p);
 #pragma unroll
-          for (int c = 0; c < PM8; ++c) zs[c * kS + rw + lane] = zr[c];
+          for (int c = 0; c < PM8; ++c) zs[c * CS + lane] = zr[c];
         }
         __syncwarp();
       }
@@ -1349,32 +1420,46 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
         for (int i = 0; i < NT * 2; ++i) {
           const int e = lane + 32 * i, c = e >> 3, r = e & 7;
           const int64_t row = r0 + rw + r;
-          if (c < p && row < P.n) P.zout[row + (int64_t)c * P.ldzout] = zs[c * kS + rw + r];
+          if (c < p && row < P.n) P.zout[row + (int64_t)c * P.ldzout] = zs[c * CS + r];
         }
       }
       if (gram_basis || gram_self) {
         double2 bz[NT];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-          bz[nt] = *reinterpret_cast<const double2*>(zs + (nt * 8 + mrow) * kS + rw + 2 * kq);
-        const double* gs = (gram_basis ? st + W.gbslot0 * kS : zs) + mrow * kS + rw + 2 * kq;
-        // all row tiles' first k-half, then the second: no back-to-back
-        // dependent DMMAs
-        double2 ga[MTA];
+          bz[nt] = *reinterpret_cast<const double2*>(zs + (nt * 8 + mrow) * CS + 2 * kq);
+        const double* gs = (gram_basis ? st + W.goff + rw : zs) + mrow * CS + 2 * kq;
+        // per chunk of row tiles: all first k-halves, then the second ones
+        // (no back-to-back dependent DMMAs); the register-resident-S
+        // variant loads its 13 tiles in two chunks to stay within 168
+        // registers
+        constexpr int GCH = KSR > 0 ? 7 : MTA;
 #pragma unroll
-        for (int mt = 0; mt < MTA; ++mt)
-          ga[mt] = mt < mtiles ? *reinterpret_cast<const double2*>(gs + mt * 8 * kS) : make_double2(0.0, 0.0);
+        for (int m0 = 0; m0 < MTA; m0 += GCH) {
+          double2 ga[GCH];
 #pragma unroll
-        for (int mt = 0; mt < MTA; ++mt)
-          if (mt < mtiles)
+          for (int j = 0; j < GCH; ++j)
+            ga[j] = (m0 + j < MTA && m0 + j < mtiles) ? *reinterpret_cast<const double2*>(gs + (m0 + j) * 8 * CS)
+                                                       : make_double2(0.0, 0.0);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma_nv(acc[mt][nt][0], acc[mt][nt][1], ga[mt].x, bz[nt].x);
+          for (int j = 0; j < GCH; ++j)
+            if (m0 + j < MTA && m0 + j < mtiles)
 #pragma unroll
-        for (int mt = 0; mt < MTA; ++mt)
-          if (mt < mtiles)
+              for (int nt = 0; nt < NT; ++nt)
+                dmma_nv(acc[m0 + j < MTA ? m0 + j : 0][nt][0], acc[m0 + j < MTA ? m0 + j : 0][nt][1], ga[j].x,
+                        bz[nt].x);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma_nv(acc[mt][nt][0], acc[mt][nt][1], ga[mt].y, bz[nt].y);
+          for (int j = 0; j < GCH; ++j)
+            if (m0 + j < MTA && m0 + j < mtiles)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt)
+                dmma_nv(acc[m0 + j < MTA ? m0 + j : 0][nt][0], acc[m0 + j < MTA ? m0 + j : 0][nt][1], ga[j].y,
+                        bz[nt].y);
+        }
       }
+      // generic-proxy writes into the stage (z write-back, solves) must be
+      // ordered before the next tensor request overwrites it
+      if (TMA && (wb || trsm)) fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == W.stages) {
@@ -1430,11 +1515,56 @@ __global__ void __launch_bounds__(WsGeom<CW>::kThreads, WsGeom<CW>::kMinBlocks) 
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
+#ifndef RG_WS_TMA
+#define RG_WS_TMA 1
+#endif
+// L2 sector promotion of the tensor requests: a 72-row box row (576 B) starts
+// at 64 B mod 128, so 256-byte promotion fetched ~8% more than the block
+// (ncu: 15.66 vs 14.50 GB for P2)
+#ifndef RG_WS_TMA_PROMO
+#define RG_WS_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_NONE
+#endif
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                      CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                      CUtensorMapFloatOOBfill);
+static TensorMapEncodeFn tensor_map_encoder() {
+  static TensorMapEncodeFn fn = []() -> TensorMapEncodeFn {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<TensorMapEncodeFn>(f);
+  }();
+  return fn;
+}
+
+// an n x ncols column-major block as a 2-D tensor {n, ncols} (row stride
+// 8 bytes, column stride ld*8), box {rows, bc}: a stage tile lands as
+// [column][rows]
+static bool encode_stage_map(CUtensorMap* m, const double* base, int64_t ld, int64_t n, int ncols, int bc,
+                             int rows) {
+  TensorMapEncodeFn enc = tensor_map_encoder();
+  if (!enc || bc > 256 || rows > 256 || ncols < 1 || n < 1) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)ncols};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {(cuuint32_t)rows, (cuuint32_t)bc};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, RG_WS_TMA_PROMO,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // the stage plan, or false when the pass is not a ws shape (triangular
-// solves, norms, two distinct terms, too many columns)
-template <int CW>
-static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem) {
-  using G = WsGeom<CW>;
+// solves, norms, two distinct terms, too many columns).  TMA: also encode the
+// tensor maps -- false when an operand cannot be described (the caller then
+// plans the cp.async variant).
+template <int CW, bool TMA>
+static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem, WsMaps* maps) {
+  using G = WsGeom<CW, TMA>;
   if (P.gmode == 3) return false;
   if (P.a2 > 0 && !P.merge12) return false;
   if (P.a1 > 4 * kWsKS) return false;
@@ -1452,8 +1582,22 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   W.ngb = (P.gmode == 1 && !alias) ? P.gc : 0;
   W.nload = W.nz + P.a1 + W.ngb;
   if (W.nload == 0) return false;
+  // below ~64 streamed columns the fixed per-stage cost (mbarrier round
+  // trips, 64-row stages) loses to v6 (profiles/ws_study_r01.txt)
+  if (W.nload < 64) return false;
+  W.stage_words = W.nslots * G::kS;
+  W.zoff = 0;
+  W.xoff = W.x1slot0 * G::kS;
+  W.goff = W.gbslot0 * G::kS;
+  W.tx = 0;
+  if (TMA) {
+    if (W.nz && !encode_stage_map(&maps->z, P.zin, P.ldzin, P.n, P.p, PM8, G::kS)) return false;
+    if (W.a1 && !encode_stage_map(&maps->x, P.x1, P.ldx1, P.n, P.a1, x1n, G::kS)) return false;
+    if (W.ngb && !encode_stage_map(&maps->g, P.gb, P.ldgb, P.n, P.gc, gbn, G::kS)) return false;
+    W.tx = (unsigned)(((W.nz ? PM8 : 0) + (W.a1 ? x1n : 0) + (W.ngb ? gbn : 0)) * G::kS * sizeof(double));
+  }
   const size_t extra = ((size_t)((P.a1 + 3) / 4) * NT * 32 + (size_t)PM8 * PM8) * sizeof(double);
-  const size_t per_stage = (size_t)W.nslots * G::kS * sizeof(double);
+  const size_t per_stage = (size_t)W.stage_words * sizeof(double);
   const size_t red_bytes = (size_t)(MT > 0 ? MT : 1) * NT * 64 * sizeof(double);
   int stages = kWsMaxStages;
   while (stages >= 2 && (size_t)stages * per_stage + extra > G::kSmemMax) --stages;
@@ -1463,18 +1607,16 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   // enough bytes in flight per SM through a ring of whole stages -- v3 / v6
   // serve them (1.15-1.2 ms vs 0.33-0.39 ms per cfg4 pass when forced here)
   if ((size_t)stages * per_stage < (size_t)96 * 1024) return false;
-  // below ~64 streamed columns the fixed per-stage cost (mbarrier round
-  // trips, 64-row stages) loses to v6 (tools/ws_sweep.py, profiles/ws_study_r01.txt)
-  if (W.nload < 64) return false;
   W.stages = stages;
   smem = (size_t)stages * per_stage + extra;
   return true;
 }
 
-template <int CW, int NT, int MT, int KSR = 0>
-static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, size_t smem, cudaStream_t st) {
-  using G = WsGeom<CW>;
-  auto k = tall_ws_kernel<CW, NT, MT, KSR>;
+template <int CW, int NT, int MT, int KSR, bool TMA>
+static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, const WsMaps& maps, size_t smem,
+                             cudaStream_t st) {
+  using G = WsGeom<CW, TMA>;
+  auto k = tall_ws_kernel<CW, NT, MT, KSR, TMA>;
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmemMax);
@@ -1484,33 +1626,53 @@ static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, size_t smem, 
   int64_t g = (int64_t)sm_count() * per_sm;
   if (nunits < g) g = nunits;
   if (g < 1) g = 1;
-  k<<<(unsigned)g, G::kThreads, smem, st>>>(P, W);
+  k<<<(unsigned)g, G::kThreads, smem, st>>>(P, W, maps);
   return cudaGetLastError();
 }
 
-template <int CW>
-static bool try_ws_cw(const TallParams& P, int NT, int MT, cudaStream_t st, cudaError_t& e) {
-  WsPlan W;
-  size_t smem = 0;
-  if (!ws_plan<CW>(P, NT, MT, W, smem)) return false;
-#define RG_WS_MT(NTv)                                                 \
-  switch (MT) {                                                       \
-    case 0: e = launch_ws<CW, NTv, 0>(P, W, smem, st); break;         \
-    case 2: e = launch_ws<CW, NTv, 2>(P, W, smem, st); break;         \
-    case 6: e = launch_ws<CW, NTv, 6>(P, W, smem, st); break;         \
-    case 13: e = launch_ws<CW, NTv, 13>(P, W, smem, st); break;       \
-    default: e = launch_ws<CW, NTv, 16>(P, W, smem, st); break;       \
+template <int CW, bool TMA>
+static void launch_ws_shape(const TallParams& P, const WsPlan& W, const WsMaps& maps, size_t smem, int NT, int MT,
+                            cudaStream_t st, cudaError_t& e) {
+#define RG_WS_MT(NTv)                                                              \
+  switch (MT) {                                                                    \
+    case 0: e = launch_ws<CW, NTv, 0, 0, TMA>(P, W, maps, smem, st); break;        \
+    case 2: e = launch_ws<CW, NTv, 2, 0, TMA>(P, W, maps, smem, st); break;        \
+    case 6: e = launch_ws<CW, NTv, 6, 0, TMA>(P, W, maps, smem, st); break;        \
+    case 13: e = launch_ws<CW, NTv, 13, 0, TMA>(P, W, maps, smem, st); break;      \
+    default: e = launch_ws<CW, NTv, 16, 0, TMA>(P, W, maps, smem, st); break;      \
   }
-  if (NT == 1 && CW == 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
+  if (NT == 1 && CW >= 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
     // the joint schedule's P2 shape at p <= 8: S in registers (3.08 -> 3.00-3.05
     // ms at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
-    e = launch_ws<CW, 1, 13, 26>(P, W, smem, st);
+    e = launch_ws<CW, 1, 13, 26, TMA>(P, W, maps, smem, st);
   } else if (NT == 1) {
     RG_WS_MT(1)
   } else {
     RG_WS_MT(2)
   }
 #undef RG_WS_MT
+}
+
+static bool try_ws_shape(const TallParams& P, int NT, int MT, cudaStream_t st, cudaError_t& e) {
+  WsPlan W;
+  WsMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  size_t smem = 0;
+  // consumer warps of the TMA variant, measured per pass type at cfg4
+  // (profiles/tma_r02.txt): 8 (2 per SMSP, 72-row boxes overlapping by 8
+  // rows) for passes with an update -- P2 2.29 ms vs 2.70 with 9 warps and
+  // 2.40 with cp.async; 9 (dense 72-row boxes) for a pure Gram -- P1 2.01 ms
+  // vs 2.13 with 8
+  if (RG_WS_TMA && P.a1 == 0 && ws_plan<9, true>(P, NT, MT, W, smem, &maps)) {
+    launch_ws_shape<9, true>(P, W, maps, smem, NT, MT, st, e);
+    return true;
+  }
+  if (RG_WS_TMA && P.a1 > 0 && ws_plan<8, true>(P, NT, MT, W, smem, &maps)) {
+    launch_ws_shape<8, true>(P, W, maps, smem, NT, MT, st, e);
+    return true;
+  }
+  if (!ws_plan<8, false>(P, NT, MT, W, smem, nullptr)) return false;
+  launch_ws_shape<8, false>(P, W, maps, smem, NT, MT, st, e);
   return true;
 }
 
@@ -1520,7 +1682,7 @@ static bool try_ws(const TallParams& P, int PM, cudaStream_t st, cudaError_t& e)
   const int NT = PM > 8 ? 2 : 1;
   const int mt = (P.gmode == 1 || P.gmode == 2) ? P.mtiles : 0;
   const int MT = mt == 0 ? 0 : (mt <= 2 ? 2 : (mt <= 6 ? 6 : (mt <= 13 ? 13 : 16)));
-  return try_ws_cw<8>(P, NT, MT, st, e);
+  return try_ws_shape(P, NT, MT, st, e);
 }
 
 // Passes without a basis Gram (update / store / self-Gram) run 4-warp CTAs

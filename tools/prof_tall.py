@@ -13,6 +13,7 @@ ap.add_argument("--a1", type=int, default=20)
 ap.add_argument("--a2", type=int, default=0)
 ap.add_argument("--gc", type=int, default=80)
 ap.add_argument("--self", action="store_true")
+ap.add_argument("--alias", action="store_true", help="Gram basis = the update operand X1 (the joint schedule's P2)")
 ap.add_argument("--store", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--trsm1", action="store_true")
@@ -25,13 +26,13 @@ def blk(c):
     b.copy_(torch.randn(n, c, generator=g, device="cuda", dtype=torch.float64))
     return b
 Z = blk(p); X1 = blk(args.a1) if args.a1 else None; X2 = blk(args.a2) if args.a2 else None
-Gb = blk(args.gc) if args.gc and not args.self else None
+Gb = (X1[:, :args.gc] if args.alias else blk(args.gc)) if args.gc and not args.self else None
 S1 = torch.randn(args.a1, p, device="cuda", dtype=torch.float64) if args.a1 else None
 S2 = torch.randn(args.a2, p, device="cuda", dtype=torch.float64) if args.a2 else None
 Zo = D.empty_block(n, p) if args.store else None
 terms = ([(X1, S1, -1.0)] if X1 is not None else []) + ([(X2, S2, -1.0)] if X2 is not None else [])
 gram = ("self", D.small(p, p)) if args.self else (("basis", Gb, D.small(args.gc, p)) if Gb is not None else None)
-cols = p + args.a1 + args.a2 + (args.gc if Gb is not None else 0) + (p if Zo is not None else 0)
+cols = p + args.a1 + args.a2 + (args.gc if Gb is not None and not args.alias else 0) + (p if Zo is not None else 0)
 if args.gc and args.a1 == args.gc and Gb is not None: pass
 R1 = torch.triu(torch.rand(p, p, device="cuda", dtype=torch.float64)) + 4 * torch.eye(p, device="cuda", dtype=torch.float64)
 r1 = R1 if (args.trsm1 or args.trsm2) else None
