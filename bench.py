@@ -357,11 +357,14 @@ def run_step(args, rank, world):
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        # the ncu launch list (tools/evidence_step.sh) captures exactly this region
+        torch.cuda.cudart().cudaProfilerStart()
         ev0.record()
         for _ in range(args.steps):
             _one_step(fact, op, rs)
         ev1.record()
         torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
     ms = ev0.elapsed_time(ev1) / args.steps
     launches = D.LaunchLog.launches()
     per_kernel = D.LaunchLog.summary()

@@ -255,6 +255,17 @@ int rg_sptrsv_perm_f64(int64_t n, const int32_t* d_rp, const int32_t* d_ci, cons
                        double* d_xw, void* d_work, int64_t work_bytes, int32_t epoch, void* stream);
 
 /*
+ * Halo pack of the row-partitioned SpMM (the reference is
+ * single-process, its product is sparse_core.py:25-40):
+ *   out[i + c*ldo] = Z[idx[i] + c*ldz],  i < k, c < p
+ * esz = 8 (float64) or 16 (complex128, ld in complex elements).  Each column
+ * of out is one contiguous send; the peer receives it straight into column c
+ * of its ghost block.
+ */
+int rg_halo_pack(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const void* d_z, int64_t ldz,
+                 void* d_out, int64_t ldo, void* stream);
+
+/*
  * Launch accounting and per-launch device timing (no reference counterpart:
  * the reference times whole Python calls with perf_counter, bench.py:58-67).
  *   rg_launch_count    kernels launched by this library since load

@@ -11,6 +11,7 @@ This reproduces the paper's §6.2 experiments on B200.
 from __future__ import annotations
 
 import csv
+import pathlib
 from dataclasses import dataclass
 
 import numpy as np
@@ -199,6 +200,48 @@ def block_single_ratios(results):
                 pts.append((L, blk.mean_seconds / (one.mean_seconds / L)))
         out[g] = pts
     return out
+
+
+_SERIES_COLORS = ("#1f3a93", "#b03a2e", "#1e8449", "#7d3c98", "#ca6f1e", "#5d6d7e")
+
+
+def emit_plot(results, path) -> None:
+    """SVG of the block / single-product time ratio against the block size L,
+    one polyline per (matrix, projector, dim_c) group (the figure the
+    reference's ``emit_plot`` draws, bench.py:212-251; drawn here with tick
+    labels on both axes and a dashed ratio-1 reference line)."""
+    series = {g: pts for g, pts in sorted(block_single_ratios(results).items()) if pts}
+    W, H, M = 640, 420, 56
+    xs = [L for pts in series.values() for L, _ in pts] or [1]
+    ys = [v for pts in series.values() for _, v in pts] or [1.0]
+    x_hi, y_hi = max(max(xs), 1), max(max(ys), 1.0)
+
+    def px(L):
+        return M + (W - 2 * M) * L / x_hi
+
+    def py(v):
+        return H - M - (H - 2 * M) * v / y_hi
+
+    el = [f'<svg xmlns="http://www.w3.org/2000/svg" width="{W}" height="{H}" font-family="sans-serif">',
+          f'<rect x="0" y="0" width="{W}" height="{H}" fill="#ffffff"/>',
+          f'<path d="M{M},{M} V{H - M} H{W - M}" fill="none" stroke="#000000"/>',
+          f'<line x1="{M}" y1="{py(1.0):.1f}" x2="{W - M}" y2="{py(1.0):.1f}" stroke="#999999" '
+          f'stroke-dasharray="4,3"/>']
+    for L in sorted(set(xs)):
+        el.append(f'<text x="{px(L):.1f}" y="{H - M + 16}" font-size="10" text-anchor="middle">{L}</text>')
+    for k in range(5):
+        v = y_hi * k / 4
+        el.append(f'<text x="{M - 6}" y="{py(v) + 3:.1f}" font-size="10" text-anchor="end">{v:.2f}</text>')
+    el.append(f'<text x="{W / 2:.0f}" y="{H - 14}" font-size="12" text-anchor="middle">block size L</text>')
+    el.append(f'<text x="{M}" y="{M - 18}" font-size="12">time(one block of L) / time(one single product)</text>')
+    for i, (g, pts) in enumerate(series.items()):
+        col = _SERIES_COLORS[i % len(_SERIES_COLORS)]
+        xy = " ".join(f"{px(L):.1f},{py(v):.1f}" for L, v in pts)
+        el.append(f'<polyline points="{xy}" fill="none" stroke="{col}" stroke-width="1.5"/>')
+        el.append(f'<text x="{W - M - 230}" y="{M + 14 * (i + 1)}" font-size="11" fill="{col}">'
+                  f'{g[0]} projector={g[1]} dim_c={g[2]}</text>')
+    el.append("</svg>")
+    pathlib.Path(path).write_text("\n".join(el) + "\n")
 
 
 def read_results_csv(path):

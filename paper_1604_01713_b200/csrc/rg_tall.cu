@@ -1209,7 +1209,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
-template <int CW, int NT, int MT, int KSR = 0, bool TMA = false>
+template <int CW, int NT, int MT, int KSR = 0, bool TMA = false, int KSM = kWsKS>
 __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>::kMinBlocks))
     tall_ws_kernel(TallParams P, WsPlan W, const __grid_constant__ WsMaps maps) {
   using G = WsGeom<CW, TMA>;
@@ -1352,7 +1352,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
     // KSR > 0: the update's S fragments (a1 <= 4*KSR, NT == 1) live in
     // registers -- a fifth of the pass's shared-memory wavefronts
     constexpr bool kBreg = KSR > 0 && NT == 1;
-    constexpr int kKS = kBreg ? KSR : kWsKS;
+    constexpr int kKS = kBreg ? KSR : KSM;  // compile-time k-steps: no predicated-off DMMAs past a1
     double bq[kBreg ? KSR : 1];
     if (kBreg) {
 #pragma unroll
@@ -1518,6 +1518,10 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
 #ifndef RG_WS_TMA
 #define RG_WS_TMA 1
 #endif
+// fewest streamed columns a TMA ws pass takes (narrower passes run on v6)
+#ifndef RG_WS_MIN_LOAD_TMA
+#define RG_WS_MIN_LOAD_TMA 64
+#endif
 // L2 sector promotion of the tensor requests: a 72-row box row (576 B) starts
 // at 64 B mod 128, so 256-byte promotion fetched ~8% more than the block
 // (ncu: 15.66 vs 14.50 GB for P2)
@@ -1584,7 +1588,7 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   if (W.nload == 0) return false;
   // below ~64 streamed columns the fixed per-stage cost (mbarrier round
   // trips, 64-row stages) loses to v6 (profiles/ws_study_r01.txt)
-  if (W.nload < 64) return false;
+  if (W.nload < (TMA ? RG_WS_MIN_LOAD_TMA : 64)) return false;
   W.stage_words = W.nslots * G::kS;
   W.zoff = 0;
   W.xoff = W.x1slot0 * G::kS;
@@ -1612,11 +1616,11 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   return true;
 }
 
-template <int CW, int NT, int MT, int KSR, bool TMA>
+template <int CW, int NT, int MT, int KSR, bool TMA, int KSM = kWsKS>
 static cudaError_t launch_ws(const TallParams& P, const WsPlan& W, const WsMaps& maps, size_t smem,
                              cudaStream_t st) {
   using G = WsGeom<CW, TMA>;
-  auto k = tall_ws_kernel<CW, NT, MT, KSR, TMA>;
+  auto k = tall_ws_kernel<CW, NT, MT, KSR, TMA, KSM>;
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmemMax);
@@ -1641,9 +1645,57 @@ static void launch_ws_shape(const TallParams& P, const WsPlan& W, const WsMaps& 
     case 13: e = launch_ws<CW, NTv, 13, 0, TMA>(P, W, maps, smem, st); break;      \
     default: e = launch_ws<CW, NTv, 16, 0, TMA>(P, W, maps, smem, st); break;      \
   }
-  if (NT == 1 && CW >= 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
-    // the joint schedule's P2 shape at p <= 8: S in registers (3.08 -> 3.00-3.05
-    // ms at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
+  const int ks1 = (P.a1 + 3) / 4;
+  bool done = false;
+  if constexpr (TMA && CW == 8) {  // (the 9-warp TMA variant serves pure Grams only)
+  done = true;
+  if (NT == 1 && P.gmode == 1 && P.a1 > 0 && !P.r1 && !P.r2 && P.mtiles >= 2 && P.mtiles <= 13 &&
+      ks1 <= 2 * P.mtiles) {
+    // P2 of the joint schedule (update by [C W] + the aliased Gram) at every
+    // basis width of a cycle: exact tile counts, S in registers.  With one
+    // 13-tile / 26-k-step instantiation the predicated-off DMMAs kept the
+    // pass at ~2.3 ms from a = 60 to a = 100 (profiles/cycle_r02_256.json)
+    switch (P.mtiles) {
+      case 2: e = launch_ws<CW, 1, 2, 4, TMA>(P, W, maps, smem, st); break;
+      case 3: e = launch_ws<CW, 1, 3, 6, TMA>(P, W, maps, smem, st); break;
+      case 4: e = launch_ws<CW, 1, 4, 8, TMA>(P, W, maps, smem, st); break;
+      case 5: e = launch_ws<CW, 1, 5, 10, TMA>(P, W, maps, smem, st); break;
+      case 6: e = launch_ws<CW, 1, 6, 12, TMA>(P, W, maps, smem, st); break;
+      case 7: e = launch_ws<CW, 1, 7, 14, TMA>(P, W, maps, smem, st); break;
+      case 8: e = launch_ws<CW, 1, 8, 16, TMA>(P, W, maps, smem, st); break;
+      case 9: e = launch_ws<CW, 1, 9, 18, TMA>(P, W, maps, smem, st); break;
+      case 10: e = launch_ws<CW, 1, 10, 20, TMA>(P, W, maps, smem, st); break;
+      case 11: e = launch_ws<CW, 1, 11, 22, TMA>(P, W, maps, smem, st); break;
+      case 12: e = launch_ws<CW, 1, 12, 24, TMA>(P, W, maps, smem, st); break;
+      default: e = launch_ws<CW, 1, 13, 26, TMA>(P, W, maps, smem, st); break;
+    }
+  } else if (NT == 1 && P.a1 > 0 && MT <= 2) {
+    // update passes (P3: merged update + self-Gram + store; R -= W (H Y)):
+    // k-steps rounded up to a multiple of 4
+#define RG_WS_KS(MTv)                                                                   \
+  switch ((ks1 + 3) / 4) {                                                              \
+    case 1: case 2: e = launch_ws<CW, 1, MTv, 0, TMA, 8>(P, W, maps, smem, st); break;  \
+    case 3: e = launch_ws<CW, 1, MTv, 0, TMA, 12>(P, W, maps, smem, st); break;         \
+    case 4: e = launch_ws<CW, 1, MTv, 0, TMA, 16>(P, W, maps, smem, st); break;         \
+    case 5: e = launch_ws<CW, 1, MTv, 0, TMA, 20>(P, W, maps, smem, st); break;         \
+    case 6: e = launch_ws<CW, 1, MTv, 0, TMA, 24>(P, W, maps, smem, st); break;         \
+    case 7: e = launch_ws<CW, 1, MTv, 0, TMA, 28>(P, W, maps, smem, st); break;         \
+    default: e = launch_ws<CW, 1, MTv, 0, TMA, 32>(P, W, maps, smem, st); break;        \
+  }
+    if (MT == 0) {
+      RG_WS_KS(0)
+    } else {
+      RG_WS_KS(2)
+    }
+#undef RG_WS_KS
+  } else {
+    done = false;
+  }
+  }
+  if (done) {
+  } else if (!TMA && NT == 1 && CW >= 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
+    // cp.async fallback of the P2 shape: S in registers (3.08 -> 3.00-3.05 ms
+    // at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
     e = launch_ws<CW, 1, 13, 26, TMA>(P, W, maps, smem, st);
   } else if (NT == 1) {
     RG_WS_MT(1)

@@ -37,6 +37,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from . import device as _dev
 
 
@@ -191,17 +192,24 @@ class CommContext:
         return t
 
     def exchange(self, sends: dict, recvs: dict):
-        """Post all sends/recvs; returns a list of works (wait() on each)."""
+        """Post all sends/recvs; returns a list of works (wait() on each).
+        Keys are peer ranks or (peer, tag) tuples; messages to one peer are
+        matched in key order on both sides."""
         ops = []
         staged = []
-        for q, buf in recvs.items():
+        peer = lambda key: key[0] if isinstance(key, tuple) else key  # noqa: E731
+        sends = dict(sorted(sends.items()))
+        recvs = dict(sorted(recvs.items()))
+        for key, buf in recvs.items():
+            q = peer(key)
             if self.nccl or not buf.is_cuda:
                 ops.append(dist.P2POp(dist.irecv, buf, q, self.group))
             else:
                 h = torch.empty(buf.shape, dtype=buf.dtype)
                 staged.append((buf, h))
                 ops.append(dist.P2POp(dist.irecv, h, q, self.group))
-        for q, buf in sends.items():
+        for key, buf in sends.items():
+            q = peer(key)
             if self.nccl or not buf.is_cuda:
                 ops.append(dist.P2POp(dist.isend, buf, q, self.group))
             else:
@@ -254,8 +262,10 @@ class DistCsr:
             self.dcsr = None
             dev = torch.device("cpu") if device is None else torch.device(device)
         self.dev = dev
-        self._send_idx = {q: torch.from_numpy(v).to(dev) for q, v in plan.send_rows.items()}
+        self._send_idx = {q: torch.from_numpy(np.ascontiguousarray(v, dtype=np.int32)).to(dev)
+                          for q, v in plan.send_rows.items()}
         self._ghost = {}
+        self._sendbuf = {}
 
     def _ghost_block(self, p, dtype):
         key = (p, dtype)
@@ -265,22 +275,43 @@ class DistCsr:
             self._ghost[key] = torch.zeros((p, ng), dtype=dtype, device=self.dev)
         return self._ghost[key]
 
+    def _pack(self, Z: torch.Tensor, q: int, idx: torch.Tensor) -> torch.Tensor:
+        """Rows ``idx`` of Z as a (p, k) contiguous buffer (column c = row c):
+        one rg_halo_pack launch on the device, index_select on the CPU path
+        of the gloo tests (local_spmm given)."""
+        p, k = Z.shape[1], idx.numel()
+        if not Z.is_cuda:
+            return Z.index_select(0, idx.long()).t().contiguous()
+        key = (q, p, Z.dtype)
+        buf = self._sendbuf.get(key)
+        if buf is None:
+            buf = self._sendbuf[key] = torch.empty((p, k), dtype=Z.dtype, device=Z.device)
+        esz = 16 if Z.dtype == torch.complex128 else 8
+        _lib.check(_dev.lib().rg_halo_pack(k, p, esz, idx.data_ptr(), Z.data_ptr(), _dev.ld_of(Z), buf.data_ptr(),
+                                           k, _dev.stream_ptr()), "halo pack")
+        return buf
+
     def apply_into(self, Z: torch.Tensor, out: torch.Tensor) -> None:
         plan = self.plan
         p = Z.shape[1]
         G = self._ghost_block(p, Z.dtype)
-        # pack: rows each peer needs, as (p, k) contiguous blocks
-        sends = {q: Z.index_select(0, idx).t().contiguous() for q, idx in self._send_idx.items()}
-        recvs = {q: torch.empty((p, s1 - s0), dtype=Z.dtype, device=self.dev)
-                 for q, (s0, s1) in plan.recv_ranges.items()}
+        # pack the rows each peer needs (one kernel per peer); every column of
+        # a send buffer is one message, received straight into the matching
+        # contiguous column segment G[c, s0:s1] of the ghost block
+        sends, recvs = {}, {}
+        for q, idx in self._send_idx.items():
+            buf = self._pack(Z, q, idx)
+            for c in range(p):
+                sends[(q, c)] = buf[c]
+        for q, (s0, s1) in plan.recv_ranges.items():
+            for c in range(p):
+                recvs[(q, c)] = G[c, s0:s1]
         works, staged = self.comm.exchange(sends, recvs) if self.comm is not None else ([], [])
         i0, i1 = plan.interior
         # interior rows need no ghost column: overlap them with the exchange
         if i1 > i0:
             self._spmm(Z, out, i0, i1, None)
         CommContext.finish(works, staged)
-        for q, (s0, s1) in plan.recv_ranges.items():
-            G[:, s0:s1].copy_(recvs[q])
         Xg = G.t()[: plan.n_ghost] if plan.n_ghost else None
         if i0 > 0:
             self._spmm(Z, out, 0, i0, Xg)

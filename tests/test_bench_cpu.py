@@ -32,3 +32,42 @@ def test_reference_arm_prints_the_step_config(capsys, monkeypatch):
     assert line["config"] == bench.step_config("cfg4", 256, 1)
     assert line["cpu_baseline"]["kind"] == "port" and line["e2e"]["h2d_bytes_per_step"] == 0
     assert np.isfinite(line["value"]) and line["value"] > 0
+
+
+def _fake_results():
+    from paper_1604_01713_b200.bench import BenchResult
+
+    out = []
+    for proj, dim_c in (("none", 0), ("cgs2", 4)):
+        for L in (1, 2, 4, 8):
+            blk = 1e-3 * (1 + 0.3 * L) * (1 + dim_c / 10)
+            one = 1e-3 * L * (1 + dim_c / 10)
+            out.append(BenchResult("cfg2", 100, 700, L, "all-at-once", proj, dim_c, 3, blk, blk, 0.0, 10 * L))
+            out.append(BenchResult("cfg2", 100, 700, L, "one-at-a-time", proj, dim_c, 3, one, one, 0.0, 10 * L))
+    return out
+
+
+def test_emit_plot_one_polyline_per_group(tmp_path):
+    """The reference's SVG contract (tests/test_bench_cli.py:97-103): an <svg>
+    document with one polyline per (matrix, projector, dim_c) group."""
+    from paper_1604_01713_b200.bench import block_single_ratios, emit_plot
+
+    res = _fake_results()
+    path = tmp_path / "ratios.svg"
+    emit_plot(res, path)
+    text = path.read_text()
+    assert text.startswith("<svg") and text.rstrip().endswith("</svg>")
+    assert text.count("<polyline") == len(block_single_ratios(res)) == 2
+    emit_plot(res, tmp_path / "again.svg")
+    assert (tmp_path / "again.svg").read_bytes() == path.read_bytes()
+
+
+def test_emit_csv_round_trip(tmp_path):
+    from paper_1604_01713_b200.bench import CSV_HEADER, emit_csv, read_results_csv
+
+    res = _fake_results()
+    emit_csv(res, tmp_path / "r.csv")
+    assert (tmp_path / "r.csv").read_text().splitlines()[0] == ",".join(CSV_HEADER)
+    back = read_results_csv(tmp_path / "r.csv")
+    assert [(r.L, r.mode, r.projector, r.dim_c, r.bytes_model) for r in back] == \
+        [(r.L, r.mode, r.projector, r.dim_c, r.bytes_model) for r in res]

@@ -3,8 +3,10 @@
 # paired with the launch labels (DRAM traffic per launch), and smoke().
 set -x
 python bench.py > gpurun_out/bench_step.json 2> gpurun_out/bench_step.err
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/ncu_launches.log 2>&1
+# launch list of the timed region only (bench.py brackets it with cudaProfilerStart/Stop)
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
+    --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-tts > gpurun_out/ncu_launches.log 2>&1
 ncu --set full --clock-control none --profile-from-start off -f -o /tmp/step \
     python tools/prof_step.py --steps 1 --labels gpurun_out/labels.json > gpurun_out/ncu_full.log 2>&1
 python tools/ncu_traffic.py /tmp/step.ncu-rep gpurun_out/labels.json gpurun_out/ncu_traffic.json

@@ -36,7 +36,9 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
     # launch order of the profiled steps (tools/ncu_traffic.py pairs it with ncu's launch list)
-    recs = [{"label": lbl, "bytes": b} for lbl, b, _, _ in D.LaunchLog.records]
+    # one record per library call; a call may launch several kernels (label repeated)
+    recs = [{"label": lbl, "bytes": b // max(nl, 1)} for lbl, _, b, _, nl in D.LaunchLog.records()
+            for _ in range(max(nl, 1))]
     D.LaunchLog.reset(timing=False)
     if args.labels:
         pathlib.Path(args.labels).write_text(json.dumps(recs, indent=1))
