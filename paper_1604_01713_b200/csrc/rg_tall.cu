@@ -1146,15 +1146,18 @@ struct WsGeom {
 
 struct WsPlan {
   int nslots, nload, x1slot0, gbslot0, stages, nz, a1, ngb;
+  // a second, distinct update term streams into the slots right after X1's
+  // (padded to x1n): the update is one k-loop over kcols = x1n + a2 columns
+  int a2, x1n, x2slot0, kcols;
   // stage layout: segment offsets (doubles) and per-consumer-warp offsets
   int stage_words;
-  int zoff, xoff, goff;  // operand segment offsets in a stage (doubles)
+  int zoff, xoff, x2off, goff;  // operand segment offsets in a stage (doubles)
   unsigned tx;           // TMA: bytes landing per stage
 };
 
 // the three operand tiles of a ws stage as 2-D tensor maps (TMA variant)
 struct WsMaps {
-  CUtensorMap z, x, g;
+  CUtensorMap z, x, x2, g;
 };
 
 
@@ -1221,7 +1224,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
   __shared__ __align__(8) uint64_t full[kWsMaxStages], empty[kWsMaxStages];
   __shared__ bool s_last;
   const int p = P.p;
-  const int ks1 = (P.a1 + 3) / 4;
+  const int ks1 = (W.kcols + 3) / 4;
   const size_t stage_words = (size_t)W.stage_words;
   double* stage0 = smem;
   double* sf1 = stage0 + (size_t)W.stages * stage_words;  // [ks1][NT][32]
@@ -1237,9 +1240,15 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
     const int ks = e / (NT * 32), nt = (e / 32) % NT, ln = e % 32;
     const int aa = ks * 4 + (ln & 3), c = nt * 8 + (ln >> 2);
     double v = 0.0;
-    if (aa < P.a1 && c < p) {
-      v = P.s1[aa + (int64_t)c * P.a1];
-      if (P.merge12) v = P.alpha1 * v + P.alpha2 * P.s2[aa + (int64_t)c * P.a2];
+    if (c < p) {
+      if (W.a2) {
+        // two distinct terms: alpha_t folded into S_t (as merge12)
+        if (aa < P.a1) v = P.alpha1 * P.s1[aa + (int64_t)c * P.a1];
+        else if (aa >= W.x1n && aa - W.x1n < P.a2) v = P.alpha2 * P.s2[(aa - W.x1n) + (int64_t)c * P.a2];
+      } else if (aa < P.a1) {
+        v = P.s1[aa + (int64_t)c * P.a1];
+        if (P.merge12) v = P.alpha1 * v + P.alpha2 * P.s2[aa + (int64_t)c * P.a2];
+      }
     }
     sf1[e] = v;
   }
@@ -1297,6 +1306,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
         mbar_expect_tx(&full[s], W.tx);
         if (W.nz) tma_tile(st + W.zoff, &maps.z, row0, &full[s]);
         if (W.a1) tma_tile(st + W.xoff, &maps.x, row0, &full[s]);
+        if (W.a2) tma_tile(st + W.x2off, &maps.x2, row0, &full[s]);
         if (W.ngb) tma_tile(st + W.goff, &maps.g, row0, &full[s]);
         if (++s == W.stages) {
           s = 0;
@@ -1333,6 +1343,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
       };
       if (W.nz) segment(P.zin, P.ldzin, W.nz, 0);
       if (W.a1) segment(P.x1, P.ldx1, W.a1, W.x1slot0);
+      if (W.a2) segment(P.x2, P.ldx2, W.a2, W.x2slot0);
       if (W.ngb) segment(P.gb, P.ldgb, W.ngb, W.gbslot0);
       cp_async_arrive_noinc(&full[s]);
       if (++s == W.stages) {
@@ -1348,7 +1359,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
     const int rw = warp * 8;
     const bool upd = P.a1 > 0;
     const bool wb = upd && (P.gmode != 0 || P.zout || trsm);
-    const double alpha = P.merge12 ? 1.0 : P.alpha1;
+    const double alpha = (P.merge12 || W.a2) ? 1.0 : P.alpha1;
     // KSR > 0: the update's S fragments (a1 <= 4*KSR, NT == 1) live in
     // registers -- a fifth of the pass's shared-memory wavefronts
     constexpr bool kBreg = KSR > 0 && NT == 1;
@@ -1520,7 +1531,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
 #endif
 // fewest streamed columns a TMA ws pass takes (narrower passes run on v6)
 #ifndef RG_WS_MIN_LOAD_TMA
-#define RG_WS_MIN_LOAD_TMA 64
+#define RG_WS_MIN_LOAD_TMA 32
 #endif
 // L2 sector promotion of the tensor requests: a 72-row box row (576 B) starts
 // at 64 B mod 128, so 256-byte promotion fetched ~8% more than the block
@@ -1570,21 +1581,27 @@ template <int CW, bool TMA>
 static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem, WsMaps* maps) {
   using G = WsGeom<CW, TMA>;
   if (P.gmode == 3) return false;
-  if (P.a2 > 0 && !P.merge12) return false;
-  if (P.a1 > 4 * kWsKS) return false;
+  const bool two = P.a2 > 0 && !P.merge12;  // a second, distinct term
+  if (two && P.a1 == 0) return false;
+  const int x1n = (P.a1 + 7) / 8 * 8;
+  const int x2n = two ? (P.a2 + 7) / 8 * 8 : 0;
+  W.a2 = two ? P.a2 : 0;
+  W.x1n = x1n;
+  W.kcols = two ? x1n + P.a2 : P.a1;
+  if (W.kcols > 4 * kWsKS) return false;
   if ((P.gmode == 1 || P.gmode == 2) && P.mtiles > MT) return false;
   if (P.gmode == 2 && P.a1 == 0 && !P.zin) return false;
   const int PM8 = NT * 8;
   const bool alias = P.gmode == 1 && P.a1 > 0 && P.gb == P.x1 && P.ldgb == P.ldx1 && P.gc <= P.a1;
-  const int x1n = (P.a1 + 7) / 8 * 8;
   const int gbn = (P.gmode == 1 && !alias) ? (P.gc + 7) / 8 * 8 : 0;
   W.x1slot0 = PM8;
-  W.gbslot0 = alias ? PM8 : PM8 + x1n;
-  W.nslots = PM8 + x1n + gbn;
+  W.x2slot0 = PM8 + x1n;
+  W.gbslot0 = alias ? PM8 : PM8 + x1n + x2n;
+  W.nslots = PM8 + x1n + x2n + gbn;
   W.nz = P.zin ? P.p : 0;
   W.a1 = P.a1;
   W.ngb = (P.gmode == 1 && !alias) ? P.gc : 0;
-  W.nload = W.nz + P.a1 + W.ngb;
+  W.nload = W.nz + P.a1 + W.a2 + W.ngb;
   if (W.nload == 0) return false;
   // below ~64 streamed columns the fixed per-stage cost (mbarrier round
   // trips, 64-row stages) loses to v6 (profiles/ws_study_r01.txt)
@@ -1592,15 +1609,17 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   W.stage_words = W.nslots * G::kS;
   W.zoff = 0;
   W.xoff = W.x1slot0 * G::kS;
+  W.x2off = W.x2slot0 * G::kS;
   W.goff = W.gbslot0 * G::kS;
   W.tx = 0;
   if (TMA) {
     if (W.nz && !encode_stage_map(&maps->z, P.zin, P.ldzin, P.n, P.p, PM8, G::kS)) return false;
     if (W.a1 && !encode_stage_map(&maps->x, P.x1, P.ldx1, P.n, P.a1, x1n, G::kS)) return false;
+    if (W.a2 && !encode_stage_map(&maps->x2, P.x2, P.ldx2, P.n, P.a2, x2n, G::kS)) return false;
     if (W.ngb && !encode_stage_map(&maps->g, P.gb, P.ldgb, P.n, P.gc, gbn, G::kS)) return false;
-    W.tx = (unsigned)(((W.nz ? PM8 : 0) + (W.a1 ? x1n : 0) + (W.ngb ? gbn : 0)) * G::kS * sizeof(double));
+    W.tx = (unsigned)(((W.nz ? PM8 : 0) + (W.a1 ? x1n : 0) + x2n + (W.ngb ? gbn : 0)) * G::kS * sizeof(double));
   }
-  const size_t extra = ((size_t)((P.a1 + 3) / 4) * NT * 32 + (size_t)PM8 * PM8) * sizeof(double);
+  const size_t extra = ((size_t)((W.kcols + 3) / 4) * NT * 32 + (size_t)PM8 * PM8) * sizeof(double);
   const size_t per_stage = (size_t)W.stage_words * sizeof(double);
   const size_t red_bytes = (size_t)(MT > 0 ? MT : 1) * NT * 64 * sizeof(double);
   int stages = kWsMaxStages;
@@ -1645,11 +1664,11 @@ static void launch_ws_shape(const TallParams& P, const WsPlan& W, const WsMaps& 
     case 13: e = launch_ws<CW, NTv, 13, 0, TMA>(P, W, maps, smem, st); break;      \
     default: e = launch_ws<CW, NTv, 16, 0, TMA>(P, W, maps, smem, st); break;      \
   }
-  const int ks1 = (P.a1 + 3) / 4;
+  const int ks1 = (W.kcols + 3) / 4;
   bool done = false;
   if constexpr (TMA && CW == 8) {  // (the 9-warp TMA variant serves pure Grams only)
   done = true;
-  if (NT == 1 && P.gmode == 1 && P.a1 > 0 && !P.r1 && !P.r2 && P.mtiles >= 2 && P.mtiles <= 13 &&
+  if (NT == 1 && P.gmode == 1 && P.a1 > 0 && W.a2 == 0 && !P.r1 && !P.r2 && P.mtiles >= 2 && P.mtiles <= 13 &&
       ks1 <= 2 * P.mtiles) {
     // P2 of the joint schedule (update by [C W] + the aliased Gram) at every
     // basis width of a cycle: exact tile counts, S in registers.  With one
@@ -1693,7 +1712,7 @@ static void launch_ws_shape(const TallParams& P, const WsPlan& W, const WsMaps& 
   }
   }
   if (done) {
-  } else if (!TMA && NT == 1 && CW >= 8 && P.a1 > 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
+  } else if (!TMA && NT == 1 && CW >= 8 && P.a1 > 0 && W.a2 == 0 && P.a1 <= 104 && MT == 13 && !P.r1 && !P.r2) {
     // cp.async fallback of the P2 shape: S in registers (3.08 -> 3.00-3.05 ms
     // at cfg4; the P3 shape was slower with it, profiles/ws_study_r01.txt)
     e = launch_ws<CW, 1, 13, 26, TMA>(P, W, maps, smem, st);
@@ -1916,7 +1935,8 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const bool aligned = aligned16(P.zin, P.ldzin) && aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) &&
                        (gram_mode != 1 || aligned16(P.gb, P.ldgb));
   if (p > 16) {
-    // wide blocks run on v6 only
+    // wide blocks run on v6 only (a 3-tile TMA ws variant measured slower for
+    // the k = 20 recycle passes: 2 stages of 78 KB, 8-lane solves -- profiles/tma_r02.txt)
     const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     RG_REQUIRE(aligned && ncol_slabs <= kMaxSlabs && (P.a1 + P.a2) <= 128,

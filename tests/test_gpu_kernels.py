@@ -235,6 +235,48 @@ def test_tall_passes_ignore_padding_rows(cuda):
                 assert np.isfinite(G.cpu().numpy()).all() and _rel(G.cpu().numpy(), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [777, 70001])
+def test_tall_recycle_update_and_solution_shapes(cuda, n):
+    """The once-per-cycle passes with two distinct update terms (staged one
+    after the other in the TMA ws stage) and three 8-column tiles (p = 20):
+    C_new = [C W] Q, U_new = ([U W_m] T) R^-1, X += W_m Y - U (F Y), and the
+    p = 20 cross Gram; NaN in every operand's padding rows."""
+    D = _dev()
+    rng = np.random.default_rng(n)
+
+    def blk(a):
+        v = D.empty_block(n, a.shape[1])
+        store = v.as_strided((D.round_ld(n), a.shape[1]), (1, D.round_ld(n)))
+        store.fill_(float("nan"))
+        v.copy_(torch.from_numpy(np.asfortranarray(a)))
+        return v
+
+    def small(a):
+        t = D.small(*a.shape)
+        t.copy_(torch.from_numpy(a))
+        return t
+
+    for p, a1, a2, trsm, zin in ((20, 20, 88, False, False), (20, 20, 80, True, False), (8, 80, 20, False, True),
+                                 (16, 40, 60, True, True)):
+        X1, X2 = rng.standard_normal((n, a1)), rng.standard_normal((n, a2))
+        S1, S2 = rng.standard_normal((a1, p)), rng.standard_normal((a2, p))
+        Z = rng.standard_normal((n, p))
+        R = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
+        Zo = D.empty_block(n, p)
+        D.tall(blk(Z) if zin else None, Zo, [(blk(X1), small(S1), 1.0), (blk(X2), small(S2), -1.0)],
+               r1=small(R) if trsm else None, n=n, p=p)
+        ref = (Z if zin else 0.0) + X1 @ S1 - X2 @ S2
+        if trsm:
+            ref = np.linalg.solve(R.T, ref.T).T
+        assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12, (p, a1, a2, trsm, zin)
+    U = rng.standard_normal((n, 20))
+    for gc in (20, 32):
+        Gb = rng.standard_normal((n, gc))
+        G = D.small(gc, 20)
+        D.tall(blk(U), None, gram=("basis", blk(Gb), G))
+        assert _rel(G.cpu().numpy(), Gb.T @ U) <= 1e-12
+
+
 def test_tall_empty_rows(cuda):
     D = _dev()
     out = D.small(3, 2)
