@@ -48,6 +48,10 @@ JOINT_PROJECTION = True
 GRAPH_MAX_ROWS = 1 << 18
 STEP_GRAPHS = False
 
+# the solver enqueues block step j+1 before reading step j's results
+# (StepPipeline); False runs the plain step-by-step order (tests compare them)
+PIPELINE_STEPS = True
+
 
 class StepWorkspace:
     """Device buffers of the factorizations of one solve, reused from cycle
@@ -74,6 +78,16 @@ class StepWorkspace:
         if b is None:
             b = self._bufs[key] = make()
         return b
+
+
+class _HostSlot:
+    """Pinned host copies of one step's small results: the packed CGS2
+    coefficients, the CholQR2 factors and its status words."""
+
+    __slots__ = ("coef", "qr", "st")
+
+    def __init__(self, coef, qr, st):
+        self.coef, self.qr, self.st = coef, qr, st
 
 
 class ZeroStartBlock(ValueError):
@@ -109,10 +123,13 @@ class ArnoldiFactorization:
             coef = torch.zeros((2 * k + 2 * wmax) * L, dtype=dtype, device=dev)
             # [C | W] in one allocation: C (copied in by start) directly precedes
             # the basis, so the CGS2 projection can treat [C W] as one basis
+            # host results of a step in two slots: the solver enqueues step j+1
+            # before it reads step j's (StepPipeline)
+            host = [_HostSlot(torch.zeros_like(coef, device="cpu").pin_memory(),
+                              torch.zeros(5 * L * L, dtype=dtype).pin_memory(),
+                              torch.zeros(2, dtype=torch.int32).pin_memory()) for _ in range(2)]
             return dict(CW=_dev.empty_block(n, k + wmax, dev, dtype), ahat=_dev.empty_block(n, L, dev, dtype),
-                        coef=coef, coef_host=torch.zeros_like(coef, device="cpu").pin_memory(),
-                        qr=QrScratch(L, dev, dtype), qr_host=torch.zeros(5 * L * L, dtype=dtype).pin_memory(),
-                        st_host=torch.zeros(2, dtype=torch.int32).pin_memory())
+                        coef=coef, host=host, qr=QrScratch(L, dev, dtype))
 
         bufs = make() if workspace is None else workspace.buffers((n, L, m_max, k, dtype, dev), make)
         self._CW = bufs["CW"]
@@ -130,11 +147,11 @@ class ArnoldiFactorization:
         # packed small coefficients of one step: S1 | c1 | S2 | c2 (column-major
         # blocks), or G1 | G2 for the joint schedule
         self._coef = bufs["coef"]
-        self._coef_host = bufs["coef_host"]
+        self._host = bufs["host"]
+        self._hb = self._host[0]  # the host slot plain step() / start() use
         self._qr = bufs["qr"]
-        self._qr_host = bufs["qr_host"]
-        self._st_host = bufs["st_host"]
         self.launches = 0  # rg_* kernel launches issued by start/step (diagnostics)
+        self._qr_fallback = False  # the last step's Q came from the host-side fallback path
 
     # ---- views (arnoldi.py:47-76)
     @property
@@ -291,28 +308,34 @@ def start(opA, R0, rank_tol: float = 1e-12, *, m_max: int, recycle=None, seed: i
     return fact
 
 
-def _qr_enqueue(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False) -> bool:
+def _qr_enqueue(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, g1_ready: bool = False,
+                hb: _HostSlot | None = None) -> bool:
     """Enqueue CholQR2 of X into Q and the D2H copies of its small results
     (no host sync).  False when the block is too wide for one CholQR2 launch
     (``_qr_collect`` then runs the TSQR / panelled path)."""
     if X.shape[1] > _dev.max_p(X):
         return False
+    hb = hb or fact._hb
     scr = fact._qr
     cholqr2_launch(X, Q, scr, g1_ready=g1_ready)
-    fact._qr_host.copy_(scr.buf, non_blocking=True)
-    fact._st_host.copy_(scr.status, non_blocking=True)
+    hb.qr.copy_(scr.buf, non_blocking=True)
+    hb.st.copy_(scr.status, non_blocking=True)
     return True
 
 
-def _qr_collect(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, enqueued: bool):
+def _qr_collect(fact: ArnoldiFactorization, X: torch.Tensor, Q: torch.Tensor, enqueued: bool,
+                hb: _HostSlot | None = None):
     """After the stream has synchronised: (R, flagged) of the CholQR2, or the
     Householder TSQR fallback when CholQR2 was not attempted or failed its
     conditioning check (dense_kernels.py:31-48 semantics either way)."""
     L = X.shape[1]
     scr = fact._qr
+    hb = hb or fact._hb
+    fact._qr_fallback = True  # Q is (re)computed below: a speculative next step is stale
     if enqueued:
-        ok, R, norm_x = cholqr2_finish(fact._qr_host.numpy(), fact._st_host.numpy(), L)
+        ok, R, norm_x = cholqr2_finish(hb.qr.numpy(), hb.st.numpy(), L)
         if ok:
+            fact._qr_fallback = False
             return R, _flags(R, norm_x, fact.rank_tol)
     else:
         if L > (_dev.MAX_P_C if X.dtype == torch.complex128 else TSQR_MAX_P):
@@ -347,7 +370,7 @@ def _capturable(opA):
     return owner
 
 
-def _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, count=True):
+def _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, count=True, hb: _HostSlot | None = None):
     """The device work of one CGS2 step up to the QR: A V_m, the projection,
     the coefficient D2H and the CholQR2 (+ its D2H).  Returns whether the QR
     was enqueued."""
@@ -388,8 +411,9 @@ def _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, count=True):
                 bases, coefs = [active, active], [c1, c2]
             project_chain(Ahat, Ahat, bases, coefs, tail_gram=("self", scr.G1) if g1 else None)
         ncoef = (2 * fact.k + 2 * (m + 1) * L) * L
-    fact._coef_host[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
-    return _qr_enqueue(fact, Ahat, Vnew, g1_ready=g1)
+    hb = hb or fact._hb
+    hb.coef[:ncoef].copy_(fact._coef[:ncoef], non_blocking=True)
+    return _qr_enqueue(fact, Ahat, Vnew, g1_ready=g1, hb=hb)
 
 
 def _replay_step(fact, opA, owner, C, m, joint):
@@ -435,6 +459,142 @@ def _replay_step(fact, opA, owner, C, m, joint):
     return enq
 
 
+class _PendingStep:
+    """A CGS2 block step whose device work is enqueued: its step index, the
+    schedule, the host slot its small results land in, the Ahat buffer it
+    projected, and an event after its last D2H copy."""
+
+    __slots__ = ("m", "joint", "enq", "hb", "ahat", "event", "C")
+
+    def __init__(self, m, joint, enq, hb, ahat, event, C):
+        self.m, self.joint, self.enq, self.hb, self.ahat, self.event, self.C = m, joint, enq, hb, ahat, event, C
+
+
+def _enqueue_cgs2(fact, opA, recycle, m, hb, ahat, graphs=False) -> _PendingStep:
+    """Enqueue block step m's device work (A V_m, CGS2 against C and the
+    basis, CholQR2 of the result into V_{m+1}, the D2H copies of its small
+    results into ``hb``) without reading any host result of step m-1."""
+    L = fact.L
+    C = recycle.c_device() if recycle is not None else None
+    k_, w_ = fact.k, (m + 1) * L
+    # [C W] as one basis when the caller certified C-orthogonality at start
+    # and C is the recycle space copied in front of W (real data; the
+    # complex tall pass has no aliased-term merge): 3 passes instead of 5
+    joint = (JOINT_PROJECTION and C is not None and k_ > 0 and fact.c_orthogonal and fact._c_src is C
+             and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
+    fused = (_dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED
+             and (joint or (k_ <= _dev.MAX_GC and w_ <= _dev.MAX_GC)))
+    owner = _capturable(opA)
+    enq = None
+    if (graphs and fused and owner is not None and fact._ws is not None and fact._ws.graphs is not None
+            and fact.n <= GRAPH_MAX_ROWS and not _dev.LaunchLog.timing and hb is fact._hb and ahat is fact._ahat):
+        enq = _replay_step(fact, opA, owner, C, m, joint)
+    if enq is None:
+        saved = fact._ahat
+        fact._ahat = ahat
+        try:
+            enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, fused, hb=hb)
+        finally:
+            fact._ahat = saved
+    ev = torch.cuda.Event()
+    ev.record()
+    return _PendingStep(m, joint, enq, hb, ahat, ev, C)
+
+
+def _collect_cgs2(fact, pend: _PendingStep):
+    """Host half of a CGS2 step once its event has completed: the R factor
+    and rank flags of the QR, and F, H accumulated as arnoldi.py:177,180,183."""
+    m, L = pend.m, fact.L
+    cols = slice(m * L, (m + 1) * L)
+    k_, w_ = fact.k, (m + 1) * L
+    R, flagged = _qr_collect(fact, pend.ahat, fact.v_block(m + 1), pend.enq, hb=pend.hb)
+    hc = pend.hb.coef.numpy()
+    if pend.joint:
+        kw = k_ + w_
+        hG1 = hc[: kw * L].reshape(L, kw).T
+        hG2 = hc[kw * L: 2 * kw * L].reshape(L, kw).T
+        fact._F[:, cols] += hG1[:k_]
+        fact._F[:, cols] += hG2[:k_]
+        fact._H[: (m + 1) * L, cols] += hG1[k_:]
+        fact._H[: (m + 1) * L, cols] += hG2[k_:]
+    else:
+        off = 0
+        blocks = []
+        for rows in (k_, w_, k_, w_):
+            blocks.append(hc[off: off + rows * L].reshape(L, rows).T)
+            off += rows * L
+        hS1, hc1, hS2, hc2 = blocks
+        if pend.C is not None:
+            fact._F[:, cols] += hS1
+            fact._F[:, cols] += hS2
+        fact._H[: (m + 1) * L, cols] += hc1
+        fact._H[: (m + 1) * L, cols] += hc2
+    return R, flagged
+
+
+class StepPipeline:
+    """Block steps of one cycle with the next step's device work enqueued
+    before the current step's small results are read on the host, so the
+    device never idles through the host half of a step (the D2H wait, F / H
+    accumulation, the progressive least squares and the stop test).
+
+    Each step is the same arithmetic as ``step``; only the host ordering
+    changes.  A speculative step is discarded -- its matvecs uncounted, its
+    basis block rewritten later -- when the current step ends the cycle or
+    changes V_{m+1} on the host side (a rank-deficient column replaced, or
+    the CholQR2 conditioning fallback).  Used for CGS2 on the solver's own
+    operator (``_Operator.apply``); other cases run ``step`` unchanged."""
+
+    def __init__(self, fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2"):
+        self.fact, self.opA, self.recycle, self.ortho = fact, opA, recycle, ortho
+        owner = getattr(opA, "__self__", None)
+        self.owner = owner if owner is not None and hasattr(owner, "count") else None
+        self.on = (PIPELINE_STEPS and ortho == "cgs2" and self.owner is not None and fact.L <= _dev.max_p(fact._ahat)
+                   and not (fact._ws is not None and fact._ws.graphs is not None))
+        self.pending = None
+        self._turn = 0
+        if self.on:
+            spare = fact._ws.buffers(("ahat2",) + tuple(fact._ahat.shape) + (fact.dtype,),
+                                     lambda: _dev.empty_block(fact.n, fact.L, fact.device, fact.dtype)) \
+                if fact._ws is not None else _dev.empty_block(fact.n, fact.L, fact.device, fact.dtype)
+            self._ahat = [fact._ahat, spare]
+
+    def _enqueue(self, m):
+        t = self._turn
+        self._turn ^= 1
+        return _enqueue_cgs2(self.fact, self.opA, self.recycle, m, self.fact._host[t], self._ahat[t])
+
+    def _discard(self, pend):
+        self.owner.count -= self.fact.L
+
+    def step(self, speculate_next: bool = True):
+        """Commit the next block step; with ``speculate_next`` the step after
+        it is enqueued first."""
+        fact = self.fact
+        if not self.on:
+            step(fact, self.opA, recycle=self.recycle, ortho=self.ortho)
+            return
+        if fact.m >= fact.m_max:
+            raise ValueError(f"factorization at capacity m_max={fact.m_max}")
+        if self.pending is None:
+            self.pending = self._enqueue(fact.m)
+        pend = self.pending
+        nxt = self._enqueue(fact.m + 1) if speculate_next and fact.m + 1 < fact.m_max else None
+        pend.event.synchronize()
+        R, flagged = _collect_cgs2(fact, pend)
+        _finish_step(fact, pend.m, R, flagged, pend.C)
+        if nxt is not None and (flagged.any() or fact._qr_fallback):
+            self._discard(nxt)  # it projected the V_{m+1} the host just replaced
+            nxt = None
+        self.pending = nxt
+
+    def close(self):
+        """Drop a speculative step the cycle did not use."""
+        if self.on and self.pending is not None:
+            self._discard(self.pending)
+            self.pending = None
+
+
 def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> ArnoldiFactorization:
     """Advance by one block step (arnoldi.py:139-193)."""
     if fact.m >= fact.m_max:
@@ -444,53 +604,28 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
     m, L = fact.m, fact.L
     cols = slice(m * L, (m + 1) * L)
     C = recycle.c_device() if recycle is not None else None
-    active = fact._W[:, : (m + 1) * L]
     Vnew = fact.v_block(m + 1)
-    k_, w_ = fact.k, (m + 1) * L
 
     if ortho == "mgs":
         _apply_operator(opA, fact.v_block(m), fact._ahat)
         _mgs_project(fact, fact._ahat, C, m, cols)
         R, flagged = _block_qr(fact, fact._ahat, Vnew)
     else:
-        # [C W] as one basis when the caller certified C-orthogonality at start
-        # and C is the recycle space copied in front of W (real data; the
-        # complex tall pass has no aliased-term merge): 3 passes instead of 5
-        joint = (JOINT_PROJECTION and C is not None and k_ > 0 and fact.c_orthogonal and fact._c_src is C
-                 and fact.dtype == torch.float64 and k_ + w_ <= _dev.MAX_GC and L <= _dev.MAX_P)
-        fused = (_dev.fused_ok() and fact.dtype == torch.float64 and L <= _dev.MAX_P_FUSED
-                 and (joint or (k_ <= _dev.MAX_GC and w_ <= _dev.MAX_GC)))
-        enq = None
-        owner = _capturable(opA)
-        if (fused and owner is not None and fact._ws is not None and fact._ws.graphs is not None
-                and fact.n <= GRAPH_MAX_ROWS and not _dev.LaunchLog.timing):
-            enq = _replay_step(fact, opA, owner, C, m, joint)
-        if enq is None:
-            enq = _cgs2_enqueue(fact, opA, owner, C, m, joint, fused)
+        pend = _enqueue_cgs2(fact, opA, recycle, m, fact._hb, fact._ahat, graphs=True)
         torch.cuda.current_stream().synchronize()  # the step's one host sync
-        R, flagged = _qr_collect(fact, fact._ahat, Vnew, enq)
-        hc = fact._coef_host.numpy()
-        if joint:
-            kw = k_ + w_
-            hG1 = hc[: kw * L].reshape(L, kw).T
-            hG2 = hc[kw * L: 2 * kw * L].reshape(L, kw).T
-            fact._F[:, cols] += hG1[:k_]
-            fact._F[:, cols] += hG2[:k_]
-            fact._H[: (m + 1) * L, cols] += hG1[k_:]
-            fact._H[: (m + 1) * L, cols] += hG2[k_:]
-        else:
-            off = 0
-            blocks = []
-            for rows in (k_, w_, k_, w_):
-                blocks.append(hc[off: off + rows * L].reshape(L, rows).T)
-                off += rows * L
-            hS1, hc1, hS2, hc2 = blocks
-            if C is not None:
-                fact._F[:, cols] += hS1
-                fact._F[:, cols] += hS2
-            fact._H[: (m + 1) * L, cols] += hc1
-            fact._H[: (m + 1) * L, cols] += hc2
+        R, flagged = _collect_cgs2(fact, pend)
 
+    _finish_step(fact, m, R, flagged, C)
+    return fact
+
+
+def _finish_step(fact, m, R, flagged, C):
+    """R into H, seeded replacement of rank-deficient columns of V_{m+1}
+    (arnoldi.py:183-190), m += 1."""
+    L = fact.L
+    cols = slice(m * L, (m + 1) * L)
+    active = fact._W[:, : (m + 1) * L]
+    Vnew = fact.v_block(m + 1)
     fact._H[(m + 1) * L: (m + 2) * L, cols] = R
     for j in np.flatnonzero(flagged):
         bases = ([C] if C is not None else []) + [active, Vnew]
@@ -502,7 +637,6 @@ def step(fact: ArnoldiFactorization, opA, recycle=None, ortho: str = "cgs2") -> 
         fact.breakdown_events.append(f"step {m + 1}: replaced rank-deficient basis column {j}"
                                      + ("" if v is not None else " (space exhausted, column zeroed)"))
     fact.m = m + 1
-    return fact
 
 
 def _mgs_project(fact, Ahat, C, m, cols):

@@ -127,16 +127,45 @@ def test_graph_replayed_steps_are_bitwise_the_eager_steps(cuda):
     systems, kw = problems.cfg1_sequence()
     runs = {}
     for graphs in (False, True):
-        old = arnoldi.STEP_GRAPHS
+        old, old_pipe = arnoldi.STEP_GRAPHS, arnoldi.PIPELINE_STEPS
         arnoldi.STEP_GRAPHS = graphs
+        arnoldi.PIPELINE_STEPS = False  # (speculative steps a cycle discards launch kernels too)
         try:
             before = D.lib().rg_launch_count()
             runs[graphs] = (solve_sequence(systems, SolverConfig(**kw)), D.lib().rg_launch_count() - before)
         finally:
-            arnoldi.STEP_GRAPHS = old
+            arnoldi.STEP_GRAPHS, arnoldi.PIPELINE_STEPS = old, old_pipe
     (eager, n_eager), (graph, n_graph) = runs[False], runs[True]
     for a, b in zip(eager, graph):
         assert a.cycles == b.cycles and a.matvec_count == b.matvec_count
         assert np.array_equal(np.concatenate(a.residual_history), np.concatenate(b.residual_history))
         assert np.array_equal(a.solution, b.solution)
     assert n_graph == n_eager  # replays report the kernels they run
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg4_32"])
+def test_pipelined_steps_are_bitwise_the_sequential_steps(cuda, case):
+    """arnoldi.StepPipeline (step j+1 enqueued before step j's results are
+    read; speculative steps discarded when a cycle ends early) changes only
+    the host ordering: identical cycles, matvec counts, residual histories and
+    solutions, bit for bit, against the plain step-by-step solve."""
+    from paper_1604_01713_b200 import SolverConfig, arnoldi, problems, solve_sequence
+
+    if case == "cfg1":
+        systems, kw = problems.cfg1_sequence()
+    else:
+        A, B, system, kw = problems.cfg4_sequence(N=32, n_systems=3)
+        systems = [(system(i), B) for i in range(3)]
+    runs = {}
+    for pipe in (False, True):
+        old = arnoldi.PIPELINE_STEPS
+        arnoldi.PIPELINE_STEPS = pipe
+        try:
+            runs[pipe] = solve_sequence(systems, SolverConfig(**kw))
+        finally:
+            arnoldi.PIPELINE_STEPS = old
+    for a, b in zip(runs[False], runs[True]):
+        assert a.error is None and b.error is None
+        assert a.cycles == b.cycles and a.matvec_count == b.matvec_count
+        assert np.array_equal(np.concatenate(a.residual_history), np.concatenate(b.residual_history))
+        assert np.array_equal(a.solution, b.solution)

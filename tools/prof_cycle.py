@@ -41,7 +41,8 @@ def main():
 
         setattr(mod, name, w)
 
-    wrap(arnoldi, "step", "arnoldi.step")
+    wrap(arnoldi, "step", "arnoldi.step")  # (the solver's cycles run arnoldi.StepPipeline)
+    wrap(solver, "_run_cycle", "cycle: start + block steps")
     wrap(arnoldi, "start", "arnoldi.start")
     wrap(solver, "_update_space", "recycle update")
     wrap(solver, "_apply_update", "apply update")
