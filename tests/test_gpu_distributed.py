@@ -48,6 +48,54 @@ def test_cfg1_sequence_two_ranks_one_gpu(cuda):
     _run(2, _cfg1_worker)
 
 
+def _nccl_entry(rank, world, port, fn):
+    import os
+    import pathlib
+    import sys
+
+    import torch
+    import torch.distributed as dist
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    sys.path.insert(0, str(root / "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    try:
+        fn(rank, world)
+    finally:
+        dist.destroy_process_group()
+
+
+def _cfg1_worker_own_gpu(rank, world):
+    import torch
+
+    from paper_1604_01713_b200 import device as D
+
+    _orig = torch.cuda.set_device
+    torch.cuda.set_device = lambda d: _orig(rank)  # the worker pins cuda:0; here each rank has its own GPU
+    try:
+        assert D.get_part() is None
+        _cfg1_worker(rank, world)
+    finally:
+        torch.cuda.set_device = _orig
+
+
+@pytest.mark.skipif("not __import__('torch').cuda.is_available() or __import__('torch').cuda.device_count() < 2",
+                    reason="needs two GPUs (one rank per GPU, NCCL halos and Gram allreduces)")
+def test_cfg1_sequence_two_gpus_nccl():
+    """The NCCL data plane: one rank per GPU, halo columns and Gram
+    allreduces over NCCL, the config-1 golden sequence reproduced."""
+    import torch.multiprocessing as mp
+
+    from test_distributed_cpu import _free_port
+
+    mp.start_processes(_nccl_entry, args=(2, _free_port(), _cfg1_worker_own_gpu), nprocs=2, join=True,
+                       start_method="spawn")
+
+
 def _cfg5_worker(rank, world):
     """Complex (config-5 shaped) sequence, row-partitioned over two ranks,
     against the same sequence solved by one process."""
