@@ -12,3 +12,4 @@ ncu --set full --clock-control none --profile-from-start off -f -o /tmp/step \
 python tools/ncu_traffic.py /tmp/step.ncu-rep gpurun_out/labels.json gpurun_out/ncu_traffic.json
 ncu -i /tmp/step.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__m_xbar2l1tex_read_bytes.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,sm__warps_active.avg.pct_of_peak_sustained_active,dram__cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active > gpurun_out/step_raw.csv
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+ncu -i /tmp/step.ncu-rep --page details --csv > gpurun_out/step_details.csv
