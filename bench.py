@@ -530,14 +530,32 @@ def solve_sequence_timed(grid, nsys, world, rank, dev):
         torch.cuda.synchronize()
         dt = _max_over_ranks(time.perf_counter() - t1, world, dev)
         rs = rs_out if rs_out is not None else rs
+        # reference-model bytes of every block step the solve ran (step j of a
+        # cycle: basis width 8(j+1); no recycle space in system 0's first cycle)
+        nnz_i = getattr(Ai, "nnz", None) or int(getattr(getattr(Ai, "plan", None), "values", np.zeros(0)).size)
+        mb = 0
+        for c, h in enumerate(rep.residual_history):
+            kk = 0 if (i == 0 and c == 0) else kw["k"]
+            mb += sum(step_model_bytes(n_glob // world, nnz_i, P_BLOCK, kk, j)[0] for j in range(len(h)))
         per.append({"system": i, "s": dt, "cycles": rep.cycles,
                     "block_steps": int(sum(len(h) for h in rep.residual_history)),
                     "matvecs": rep.matvec_count, "converged": bool(rep.converged),
-                    "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms))})
+                    "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms)),
+                    "step_model_bytes": mb * world})
     D.set_comm(None, None)
+    total_s = sum(r["s"] for r in per)
+    total_steps = sum(r["block_steps"] for r in per)
+    bsz = n_glob * P_BLOCK * 8
     return {"s_per_system": statistics.mean(r["s"] for r in per), "systems": per, "setup_s": t_setup,
             "workload": f"cfg4 sequence {grid}^3 conv-diff beta=20, p=8, m=10, k=20, tol 1e-8, {nsys} systems",
-            "n_gpus": world}
+            "n_gpus": world,
+            # the step metric end to end through the public solve API: host B in,
+            # host X out, every cycle operation inside the time (numerator: the
+            # block steps' reference-model bytes only)
+            "e2e_solve": {"value": sum(r["step_model_bytes"] for r in per) / total_s / 1e9, "unit": "GB/s",
+                          "path": "solve_block_gcrodr(CsrMatrix, host B) -> host X per system",
+                          "h2d_bytes_per_step": nsys * bsz / max(total_steps, 1),
+                          "d2h_bytes_per_step": nsys * bsz / max(total_steps, 1)}}
 
 
 def run_solve(args, rank, world):
@@ -558,7 +576,7 @@ def run_solve(args, rank, world):
                           "data": "synthetic",
                           "config": {"workload": rec["workload"], "setup_s": rec["setup_s"],
                                      "parallelism": f"row-partition x{world}"},
-                          "systems": rec["systems"]}), flush=True)
+                          "e2e_solve": rec["e2e_solve"], "systems": rec["systems"]}), flush=True)
 
 
 def _run_solve_cfg5(args, rank, world):
