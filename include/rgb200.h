@@ -279,6 +279,8 @@ int rg_halo_pack(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const 
  *   rg_profile_record  record i: label, device ms (synchronises on its end
  *                      event), algorithmic bytes, FP64
  *                      tensor-core flops, kernels launched
+ *   rg_profile_gap     device ms from the end of record i-1 to the start of
+ *                      record i (work of other libraries + idle time)
  */
 int64_t rg_launch_count(void);
 void rg_count_launches(int64_t n);
@@ -286,6 +288,7 @@ void rg_profile_enable(int32_t on);
 int32_t rg_profile_count(void);
 int rg_profile_record(int32_t i, char* label, int32_t label_cap, double* ms, int64_t* bytes, double* flops,
                       int32_t* launches);
+int rg_profile_gap(int32_t i, double* ms);
 
 #ifdef __cplusplus
 }

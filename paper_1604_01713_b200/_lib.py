@@ -69,6 +69,7 @@ PROTOTYPES = {
     "rg_profile_count": (c_i32, []),
     "rg_profile_record": (ctypes.c_int, [c_i32, ctypes.c_char_p, c_i32, ctypes.POINTER(c_dbl),
                                          ctypes.POINTER(c_i64), ctypes.POINTER(c_dbl), ctypes.POINTER(c_i32)]),
+    "rg_profile_gap": (ctypes.c_int, [c_i32, ctypes.POINTER(c_dbl)]),
 }
 
 _lib = None

@@ -151,3 +151,27 @@ extern "C" int rg_profile_record(int32_t i, char* label, int32_t label_cap, doub
   }
   return RG_OK;
 }
+
+// device time between the end of record i-1 and the start of record i: torch
+// plumbing between library calls plus idle time (host latency) -- the
+// timeline gaps tools/prof_gaps.py attributes to solver phases
+extern "C" int rg_profile_gap(int32_t i, double* ms) {
+  using namespace rg;
+  clear_error();
+  cudaEvent_t a, b;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    RG_REQUIRE(i >= 1 && i < (int32_t)g_recs.size(), "rg_profile_gap: index %d of %d", i, (int)g_recs.size());
+    a = g_recs[i - 1].e1;
+    b = g_recs[i].e0;
+  }
+  cudaError_t e = cudaEventSynchronize(b);
+  float t = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, a, b);
+  if (e != cudaSuccess) {
+    set_error("rg_profile_gap: %s", cudaGetErrorString(e));
+    return RG_ECUDA;
+  }
+  *ms = t;
+  return RG_OK;
+}

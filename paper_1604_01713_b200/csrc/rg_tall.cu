@@ -1123,7 +1123,10 @@ static cudaError_t launch_v6(const TallParams& P, int64_t max_grid, cudaStream_t
 // ============================================================================
 
 constexpr int kWsKS = 32;  // update k-steps (a1 <= 128)
-constexpr int kWsMaxStages = 8;
+#ifndef RG_WS_MAX_STAGES
+#define RG_WS_MAX_STAGES 8
+#endif
+constexpr int kWsMaxStages = RG_WS_MAX_STAGES;  // ring depth cap (narrow passes need deep rings)
 constexpr size_t kWsSmemMax = 220 * 1024;
 
 #ifndef RG_WS_PROD8

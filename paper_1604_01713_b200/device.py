@@ -117,6 +117,22 @@ def small(rows: int, cols: int, device=None, dtype=torch.float64) -> torch.Tenso
     return torch.empty((max(cols, 1), max(rows, 1)), dtype=dtype, device=dev).t()[:rows, :cols]
 
 
+def upload_small(a: np.ndarray, device=None) -> torch.Tensor:
+    """A small host matrix (coefficients) on the device without stalling the
+    stream: staged through pinned memory and copied asynchronously, so the
+    host does not wait for the queued kernels to drain (a pageable
+    ``torch.from_numpy(a).to(dev)`` synchronises the stream first).  The
+    result is column-major with ld = rows, like ``small``."""
+    dev = require_cuda(device)
+    a = np.asarray(a)
+    if a.ndim == 1:
+        a = a.reshape(-1, 1)
+    host = torch.empty((a.shape[1], a.shape[0]), dtype=torch.complex128 if np.iscomplexobj(a) else torch.float64,
+                       pin_memory=True)
+    host.numpy()[...] = a.T
+    return host.to(dev, non_blocking=True).t()
+
+
 def ld_of(t: torch.Tensor) -> int:
     n = t.shape[0]
     if t.dim() == 1:
