@@ -65,6 +65,25 @@ int rg_spmm_csr_f64(int64_t n_rows, int64_t row_begin, int64_t row_end,
                     int32_t p, double* d_y, int64_t ldy, void* stream);
 
 /*
+ * The same product for matrices whose nonzeros lie on <= 32 diagonals (the
+ * stencil configurations), from a diagonal layout built once per matrix:
+ *   d_dia   n_rows x ndiag column-major (ld_dia), value of row i on diagonal
+ *           h_offsets[d] (column i + h_offsets[d]), 0 where i stores none
+ *   d_mask  n_rows uint32 bit masks: bit d set iff row i stores that entry
+ *   h_offsets ascending (host array)
+ * Each row sums its stored entries in ascending column order with the
+ * reference's separately rounded arithmetic: bitwise equal to
+ * rg_spmm_csr_f64 on the same matrix.  X windows per block of rows stream in
+ * by TMA; no column indices are read.  d_row_ptr (optional) is the CSR row
+ * pointer, used only for the launch record's byte model.  Requires 16-byte
+ * aligned operands with even leading dimensions; no ghost columns.
+ */
+int rg_spmm_dia_f64(int64_t n_rows, int64_t row_begin, int64_t row_end, int32_t ndiag, const int32_t* h_offsets,
+                    const double* d_dia, int64_t ld_dia, const uint32_t* d_mask, int64_t n_cols,
+                    const double* d_x, int64_t ldx, int32_t p, double* d_y, int64_t ldy, const int32_t* d_row_ptr,
+                    void* stream);
+
+/*
  * Fused tall-skinny "update, triangular solve, Gram" pass over an n x p
  * block Z (one read of every operand, one write of Z):
  *

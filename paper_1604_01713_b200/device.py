@@ -303,6 +303,11 @@ class LaunchLog:
 # ---------------------------------------------------------------------------
 
 
+# stencil-like matrices run on the diagonal-layout SpMM (rg_spmm_dia_f64);
+# False keeps every product on the CSR kernel (tests compare the two)
+SPMM_DIA = True
+
+
 def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: int | None = None,
          n_local: int | None = None, Xg: torch.Tensor | None = None) -> torch.Tensor:
     """Y[rows] = A[rows] @ X (bitwise the reference kernel's arithmetic)."""
@@ -314,6 +319,15 @@ def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: in
     cplx = X.dtype == torch.complex128
     if cplx != (dcsr.values.dtype == torch.complex128) or Y.dtype != X.dtype:
         raise TypeError(f"spmm: matrix values {dcsr.values.dtype}, block {X.dtype}, output {Y.dtype} must agree")
+    plan = dcsr.dia() if (not cplx and Xg is None and SPMM_DIA and hasattr(dcsr, "dia")) else None
+    if plan is not None and X.numel() and is_col_major(X) and ld_of(X) % 2 == 0 and X.data_ptr() % 16 == 0:
+        # stencil-like matrix: the diagonal-layout kernel (same arithmetic, bitwise)
+        offs = plan.offsets
+        rc = L.rg_spmm_dia_f64(n_rows, row_begin, row_end, len(offs), offs.ctypes.data, plan.dia.data_ptr(),
+                               ld_of(plan.dia), plan.mask.data_ptr(), n_local, X.data_ptr(), ld_of(X), p,
+                               Y.data_ptr(), ld_of(Y), dcsr.row_ptr.data_ptr(), stream_ptr())
+        _lib.check(rc, "spmm (dia)")
+        return Y
     fn = L.rg_spmm_csr_c128 if cplx else L.rg_spmm_csr_f64
     rc = fn(n_rows, row_begin, row_end, dcsr.row_ptr.data_ptr(), dcsr.col_idx.data_ptr(),
             dcsr.values.data_ptr(), X.data_ptr() if X.numel() else None, ld_of(X), n_local,

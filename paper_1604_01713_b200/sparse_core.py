@@ -57,7 +57,7 @@ class DeviceCsr:
     """CSR arrays resident in HBM: int32 row_ptr (n+1), int32 col_idx and
     float64 values (nnz), in the host matrix's storage order."""
 
-    __slots__ = ("n_rows", "n_cols", "nnz", "row_ptr", "col_idx", "values", "device", "host_row_ptr")
+    __slots__ = ("n_rows", "n_cols", "nnz", "row_ptr", "col_idx", "values", "device", "host_row_ptr", "_dia")
 
     def __init__(self, n_rows, n_cols, row_ptr, col_idx, values, device):
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
@@ -67,6 +67,16 @@ class DeviceCsr:
         self.values = values
         self.nnz = int(values.shape[0])
         self.host_row_ptr = None
+        self._dia = False  # not yet analysed; None: not a diagonal matrix
+
+    def dia(self):
+        """The diagonal layout of this matrix (``DiaPlan``), built on the
+        device on first use, or None when its nonzeros do not lie on a few
+        well-filled diagonals (the CSR kernel then runs)."""
+        if self._dia is False:
+            self._dia = DiaPlan.build(self)
+        return self._dia
+
 
     @classmethod
     def from_host(cls, n_rows, n_cols, row_ptr, col_idx, values, device=None):
@@ -80,6 +90,45 @@ class DeviceCsr:
         out = cls(n_rows, n_cols, rp, ci, v, dev)
         out.host_row_ptr = np.asarray(row_ptr)
         return out
+
+
+class DiaPlan:
+    """Diagonal layout of a DeviceCsr for rg_spmm_dia_f64 (the stencil
+    matrices of BASELINE configs[0]-[3]): ascending offsets (host int32), the
+    values as an n_rows x ndiag column-major block (zero where a row stores no
+    entry on that diagonal) and per-row bit masks of the stored entries.
+    Summing each row's masked entries in ascending offset order is the CSR
+    row's ascending column order, so the product stays bitwise the
+    reference's."""
+
+    MAX_DIAG = 32
+    MAX_FILL = 1.25  # ndiag * n_rows <= MAX_FILL * nnz
+
+    __slots__ = ("offsets", "dia", "mask")
+
+    def __init__(self, offsets, dia, mask):
+        self.offsets, self.dia, self.mask = offsets, dia, mask
+
+    @classmethod
+    def build(cls, A: "DeviceCsr"):
+        if A.values.dtype != torch.float64 or A.nnz == 0 or A.n_rows == 0:
+            return None
+        dev = A.device
+        counts = (A.row_ptr[1:] - A.row_ptr[:-1]).long()
+        rows = torch.repeat_interleave(torch.arange(A.n_rows, device=dev), counts)
+        off = A.col_idx.long() - rows
+        uniq = torch.unique(off)
+        nd = int(uniq.numel())
+        if nd > cls.MAX_DIAG or nd * A.n_rows > cls.MAX_FILL * A.nnz:
+            return None
+        d = torch.searchsorted(uniq, off)
+        dia = _dev.zeros_block(A.n_rows, nd, dev)
+        dia.index_put_((rows, d), A.values)
+        mask = torch.zeros(_dev.round_ld(A.n_rows), dtype=torch.int32, device=dev)
+        mask.index_add_(0, rows, torch.bitwise_left_shift(torch.ones_like(d), d).to(torch.int32))
+        offsets = np.ascontiguousarray(uniq.cpu().numpy(), dtype=np.int32)
+        del counts, rows, off, d
+        return cls(offsets, dia, mask)
 
 
 def _validate(n_rows, n_cols, rp, ci, v):

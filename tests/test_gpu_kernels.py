@@ -459,3 +459,44 @@ def test_c_abi_cgs2_joint_schedule(cuda):
     rc = L.rg_cgs2_f64(n, p, Zd.data_ptr(), D.ld_of(Zd), CW.data_ptr(), D.ld_of(CW), k, Wsep.data_ptr(),
                        D.ld_of(Wsep), w, coef.data_ptr(), None, 1, ws.data_ptr(), ws.numel(), D.stream_ptr())
     assert rc == _lib.RG_EBADARG
+
+
+@pytest.mark.parametrize("case", ["cfg1_2d", "cfg2_lap32", "cd3d_48", "banded_ragged"])
+@pytest.mark.parametrize("p", [1, 3, 8, 13])
+def test_spmm_diagonal_layout_bitwise(cuda, case, p):
+    """rg_spmm_dia_f64 (the stencil matrices' diagonal layout, TMA row
+    windows) against rg_spmm_csr_f64 and the oracle: bitwise, including rows
+    with missing diagonals, row ranges, and +-inf in X columns a row does not
+    reference (a zero-padded diagonal slot must not turn them into NaN)."""
+    import oracle
+    from paper_1604_01713_b200 import device as D, problems
+    from paper_1604_01713_b200.sparse_core import gen_banded
+
+    A = {"cfg1_2d": lambda: problems.conv_diff_2d(64, 10.0), "cfg2_lap32": lambda: problems.laplacian_3d(32),
+         "cd3d_48": lambda: problems.conv_diff_3d(48, 20.0), "banded_ragged": lambda: gen_banded(5000, 3, 7)}[case]()
+    dA = A.device(cuda)
+    plan = dA.dia()
+    if case != "banded_ragged":
+        assert plan is not None and len(plan.offsets) <= 27
+    rng = np.random.default_rng(p)
+    X = rng.standard_normal((A.n_cols, p))
+    if case == "cfg1_2d":
+        X[0, :] = np.inf  # row 0's column: rows not referencing it must stay finite
+    Xd = D.to_device_block(X)
+    Yd = D.empty_block(A.n_rows, p)
+    old = D.SPMM_DIA
+    try:
+        D.SPMM_DIA = True
+        D.spmm(dA, Xd, Yd)
+        y_dia = D.to_numpy_block(Yd)
+        D.spmm(dA, Xd, Yd, 17, A.n_rows - 5)  # row range: rows outside keep the full product
+        y_rng = D.to_numpy_block(Yd)
+        D.SPMM_DIA = False
+        D.spmm(dA, Xd, Yd)
+        y_csr = D.to_numpy_block(Yd)
+    finally:
+        D.SPMM_DIA = old
+    ref = oracle.spmm(A.row_ptr, A.col_idx, A.values, X)
+    assert np.array_equal(y_csr, ref, equal_nan=True)
+    assert np.array_equal(y_dia, ref, equal_nan=True)
+    assert np.array_equal(y_rng, ref, equal_nan=True)

@@ -21,7 +21,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--systems", type=int, default=2)
+    ap.add_argument("--no-dia", action="store_true", help="keep every SpMM on the CSR kernel")
     args = ap.parse_args()
+    from paper_1604_01713_b200 import device as D
+
+    D.SPMM_DIA = not args.no_dia
     dev = torch.device("cuda", 0)
     out = {}
     for run in ("cold", "warm"):
