@@ -1360,17 +1360,23 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
     // (stage row r, column c) of an operand segment is at seg[c * CS + r]
     const int mrow = lane >> 2, kq = lane & 3;
     const int rw = warp * 8;
-    const bool upd = P.a1 > 0;
+    // (the 9-warp TMA variant and the 7-warp Gram variants carry no update code)
+    constexpr bool kUpdCode = !(TMA && CW == 9) && !(CW == 7 && MT > 0);
+    const bool upd = kUpdCode && P.a1 > 0;
     const bool wb = upd && (P.gmode != 0 || P.zout || trsm);
     const double alpha = (P.merge12 || W.a2) ? 1.0 : P.alpha1;
     // KSR > 0: the update's S fragments (a1 <= 4*KSR, NT == 1) live in
     // registers -- a fifth of the pass's shared-memory wavefronts
-    constexpr bool kBreg = KSR > 0 && NT == 1;
+    // (also the three-tile updates without a Gram: 3 x KSR fragments)
+    constexpr bool kBreg = KSR > 0 && (NT == 1 || MT == 0);
     constexpr int kKS = kBreg ? KSR : KSM;  // compile-time k-steps: no predicated-off DMMAs past a1
-    double bq[kBreg ? KSR : 1];
+    double bq[kBreg ? KSR : 1][kBreg ? NT : 1];
     if (kBreg) {
 #pragma unroll
-      for (int ks = 0; ks < (kBreg ? KSR : 1); ++ks) bq[ks] = ks < ks1 ? sf1[ks * 32 + lane] : 0.0;
+      for (int ks = 0; ks < (kBreg ? KSR : 1); ++ks)
+#pragma unroll
+        for (int nt = 0; nt < (kBreg ? NT : 1); ++nt)
+          bq[ks][nt] = ks < ks1 ? sf1[(ks * NT + nt) * 32 + lane] : 0.0;
     }
     int s = 0;
     unsigned ph = 0;
@@ -1397,7 +1403,7 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
               dmma_nv(m[ks % kWsNacc][nt][0], m[ks % kWsNacc][nt][1], a,
-                      kBreg ? bq[kBreg ? ks : 0] : sf1[(ks * NT + nt) * 32 + lane]);
+                      kBreg ? bq[kBreg ? ks : 0][kBreg ? nt : 0] : sf1[(ks * NT + nt) * 32 + lane]);
           }
         }
 #pragma unroll
@@ -1446,8 +1452,8 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
         // per chunk of row tiles: all first k-halves, then the second ones
         // (no back-to-back dependent DMMAs); the register-resident-S
         // variant loads its 13 tiles in two chunks to stay within 168
-        // registers
-        constexpr int GCH = KSR > 0 ? 7 : MTA;
+        // registers; so do the three-tile Grams (14 tiles x 3 fragments)
+        constexpr int GCH = (KSR > 0 || (NT == 3 && MTA > 7)) ? 7 : MTA;
 #pragma unroll
         for (int m0 = 0; m0 < MTA; m0 += GCH) {
           double2 ga[GCH];
@@ -1532,6 +1538,12 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
 #ifndef RG_WS_TMA
 #define RG_WS_TMA 1
 #endif
+// consumer warps of the three-tile (p = 17..24) update passes: 7 (+ the
+// producer: 8 warps, 255 registers, S fragments in registers) or 8 (+1: 168
+// registers, S fragments read from shared memory)
+#ifndef RG_WS_NT3_UPD_CW
+#define RG_WS_NT3_UPD_CW 7
+#endif
 // fewest streamed columns a TMA ws pass takes (narrower passes run on v6)
 #ifndef RG_WS_MIN_LOAD_TMA
 #define RG_WS_MIN_LOAD_TMA 32
@@ -1597,10 +1609,14 @@ static bool ws_plan(const TallParams& P, int NT, int MT, WsPlan& W, size_t& smem
   const int PM8 = NT * 8;
   const bool alias = P.gmode == 1 && P.a1 > 0 && P.gb == P.x1 && P.ldgb == P.ldx1 && P.gc <= P.a1;
   const int gbn = (P.gmode == 1 && !alias) ? (P.gc + 7) / 8 * 8 : 0;
-  W.x1slot0 = PM8;
-  W.x2slot0 = PM8 + x1n;
-  W.gbslot0 = alias ? PM8 : PM8 + x1n + x2n;
-  W.nslots = PM8 + x1n + x2n + gbn;
+  // no Zin to stage: z is written back over the warp's own rows of the first
+  // update operand (read completely by then) -- one slot group fewer per stage
+  // (the p = 20 recycle passes: 3 stages instead of 2)
+  const int zslots = (!P.zin && P.a1 > 0 && x1n >= PM8 && !alias) ? 0 : PM8;
+  W.x1slot0 = zslots;
+  W.x2slot0 = zslots + x1n;
+  W.gbslot0 = alias ? zslots : zslots + x1n + x2n;
+  W.nslots = zslots + x1n + x2n + gbn;
   W.nz = P.zin ? P.p : 0;
   W.a1 = P.a1;
   W.ngb = (P.gmode == 1 && !alias) ? P.gc : 0;
@@ -1669,6 +1685,43 @@ static void launch_ws_shape(const TallParams& P, const WsPlan& W, const WsMaps& 
   }
   const int ks1 = (W.kcols + 3) / 4;
   bool done = false;
+  if (NT == 3) {
+    // p = 17..24 (the k = 20 recycle passes), TMA only: pure Grams of a
+    // block against up to 128 basis columns (the cross Grams [C W]^T U), and
+    // updates without a Gram or solve (C_new = [C W] Q, U_new = [U W_m] T')
+    e = cudaErrorInvalidConfiguration;  // try_ws screens other shapes out
+    if constexpr (TMA && CW == 7) {
+      if (P.a1 == 0 && MT > 0) {
+        switch (MT) {
+          case 3: e = launch_ws<CW, 3, 3, 0, TMA>(P, W, maps, smem, st); break;
+          case 14: e = launch_ws<CW, 3, 14, 0, TMA>(P, W, maps, smem, st); break;
+          default: e = launch_ws<CW, 3, 16, 0, TMA>(P, W, maps, smem, st); break;
+        }
+      }
+    }
+    if constexpr (TMA && CW == RG_WS_NT3_UPD_CW) {
+      if (P.a1 > 0 && MT == 0) {
+        // 7 warps: S fragments in registers, exact k-steps for the recycle shapes:
+        // [C W] Q (108 -> 27), [U W_m] T' (24 + 80 -> 26), first cycle W Q (88 -> 22), W_m T' (80 -> 20);
+        // 8 warps: S fragments from shared memory, k-steps rounded up to 4
+        if constexpr (CW != 7) {
+          switch ((ks1 + 3) / 4) {
+            case 1: case 2: case 3: case 4: case 5: e = launch_ws<CW, 3, 0, 0, TMA, 20>(P, W, maps, smem, st); break;
+            case 6: e = launch_ws<CW, 3, 0, 0, TMA, 24>(P, W, maps, smem, st); break;
+            case 7: e = launch_ws<CW, 3, 0, 0, TMA, 28>(P, W, maps, smem, st); break;
+            default: e = launch_ws<CW, 3, 0, 0, TMA, 32>(P, W, maps, smem, st); break;
+          }
+        } else if (ks1 <= 20) e = launch_ws<CW, 3, 0, 20, TMA>(P, W, maps, smem, st);
+        else if (ks1 <= 22) e = launch_ws<CW, 3, 0, 22, TMA>(P, W, maps, smem, st);
+        else if (ks1 <= 24) e = launch_ws<CW, 3, 0, 24, TMA>(P, W, maps, smem, st);
+        else if (ks1 <= 26) e = launch_ws<CW, 3, 0, 26, TMA>(P, W, maps, smem, st);
+        else if (ks1 <= 27) e = launch_ws<CW, 3, 0, 27, TMA>(P, W, maps, smem, st);
+        else if (ks1 <= 28) e = launch_ws<CW, 3, 0, 28, TMA>(P, W, maps, smem, st);
+        else e = launch_ws<CW, 3, 0, 0, TMA, 32>(P, W, maps, smem, st);
+      }
+    }
+    return;
+  }
   if constexpr (TMA && CW == 8) {  // (the 9-warp TMA variant serves pure Grams only)
   done = true;
   if (NT == 1 && P.gmode == 1 && P.a1 > 0 && W.a2 == 0 && !P.r1 && !P.r2 && P.mtiles >= 2 && P.mtiles <= 13 &&
@@ -1737,7 +1790,17 @@ static bool try_ws_shape(const TallParams& P, int NT, int MT, cudaStream_t st, c
   // rows) for passes with an update -- P2 2.29 ms vs 2.70 with 9 warps and
   // 2.40 with cp.async; 9 (dense 72-row boxes) for a pure Gram -- P1 2.01 ms
   // vs 2.13 with 8
-  if (RG_WS_TMA && P.a1 == 0 && ws_plan<9, true>(P, NT, MT, W, smem, &maps)) {
+  if (RG_WS_TMA && NT == 3 && P.a1 > 0 && ws_plan<RG_WS_NT3_UPD_CW, true>(P, NT, MT, W, smem, &maps)) {
+    launch_ws_shape<RG_WS_NT3_UPD_CW, true>(P, W, maps, smem, NT, MT, st, e);
+    return true;
+  }
+  if (RG_WS_TMA && NT == 3 && P.a1 == 0 && ws_plan<7, true>(P, NT, MT, W, smem, &maps)) {
+    // three-tile Grams hold 14 x 3 DMMA fragments per lane: 7 consumer warps +
+    // the producer (8 warps, 255 registers) instead of 9 + 1 (168, spills)
+    launch_ws_shape<7, true>(P, W, maps, smem, NT, MT, st, e);
+    return true;
+  }
+  if (RG_WS_TMA && NT < 3 && P.a1 == 0 && ws_plan<9, true>(P, NT, MT, W, smem, &maps)) {
     launch_ws_shape<9, true>(P, W, maps, smem, NT, MT, st, e);
     return true;
   }
@@ -1745,6 +1808,7 @@ static bool try_ws_shape(const TallParams& P, int NT, int MT, cudaStream_t st, c
     launch_ws_shape<8, true>(P, W, maps, smem, NT, MT, st, e);
     return true;
   }
+  if (NT == 3) return false;  // three-tile blocks: TMA variants only (else v6)
   if (!ws_plan<8, false>(P, NT, MT, W, smem, nullptr)) return false;
   launch_ws_shape<8, false>(P, W, maps, smem, NT, MT, st, e);
   return true;
@@ -1752,9 +1816,15 @@ static bool try_ws_shape(const TallParams& P, int NT, int MT, cudaStream_t st, c
 
 // returns false when the pass is not a ws shape (caller falls back to v6)
 static bool try_ws(const TallParams& P, int PM, cudaStream_t st, cudaError_t& e) {
-  if (PM > 16) return false;
-  const int NT = PM > 8 ? 2 : 1;
+  if (PM > 24) return false;
+  const int NT = PM > 16 ? 3 : (PM > 8 ? 2 : 1);
   const int mt = (P.gmode == 1 || P.gmode == 2) ? P.mtiles : 0;
+  if (NT == 3) {
+    // pure Grams (gram modes 1/2, no update) or plain updates (no Gram); no solves
+    if (P.r1 || P.r2 || P.gmode == 3) return false;
+    if (!((P.a1 == 0 && mt > 0) || (P.a1 > 0 && mt == 0))) return false;
+    return try_ws_shape(P, NT, mt == 0 ? 0 : (mt <= 3 ? 3 : (mt <= 14 ? 14 : 16)), st, e);
+  }
   const int MT = mt == 0 ? 0 : (mt <= 2 ? 2 : (mt <= 6 ? 6 : (mt <= 13 ? 13 : 16)));
   return try_ws_shape(P, NT, MT, st, e);
 }
@@ -1886,8 +1956,12 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   clear_error();
   RG_REQUIRE(n >= 0, "rg_tall_f64: n=%lld < 0", (long long)n);
   RG_REQUIRE(p >= 1 && p <= 32, "rg_tall_f64: block width p=%d outside [1, 32]", p);
-  RG_REQUIRE(p <= 16 || gram_mode == 0 || gram_mode == 3 || gc <= (p <= 24 ? 32 : 16),
-             "rg_tall_f64: Gram basis width gc=%d too wide for p=%d (32 for p <= 24, 16 above)", gc, p);
+  // p = 17..24: a pure basis Gram takes up to 128 columns (ws, TMA), else 32
+  const bool wide_pure_gram = p <= 24 && gram_mode == 1 && a1 == 0 && a2 == 0 && !d_r1 && !d_r2 && !d_zout;
+  RG_REQUIRE(p <= 16 || gram_mode == 0 || gram_mode == 3 || gc <= (p <= 24 ? 32 : 16) ||
+                 (wide_pure_gram && gc <= 128),
+             "rg_tall_f64: Gram basis width gc=%d too wide for p=%d (32 for p <= 24, 128 for a pure Gram, 16 "
+             "above)", gc, p);
   RG_REQUIRE(a1 >= 0 && a2 >= 0 && a1 + a2 <= 512, "rg_tall_f64: term widths %d, %d", a1, a2);
   RG_REQUIRE(!d_zin || ldzin >= n, "rg_tall_f64: ldzin < n");
   RG_REQUIRE(!d_zout || ldzout >= n, "rg_tall_f64: ldzout < n");
@@ -1938,8 +2012,23 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   const bool aligned = aligned16(P.zin, P.ldzin) && aligned16(P.x1, P.ldx1) && aligned16(P.x2, P.ldx2) &&
                        (gram_mode != 1 || aligned16(P.gb, P.ldgb));
   if (p > 16) {
-    // wide blocks run on v6 only (a 3-tile TMA ws variant measured slower for
-    // the k = 20 recycle passes: 2 stages of 78 KB, 8-lane solves -- profiles/tma_r02.txt)
+    // p = 17..24 without solves: the three-tile TMA ws kernel (pure Grams up to
+    // 128 basis columns; updates staging z over the first operand's rows, so
+    // 3 stages fit).  The earlier 3-tile attempt with 2 stages of 78 KB and
+    // 8-lane solves measured slower (profiles/tma_r02.txt); solves stay on v6.
+    if (aligned && PM == 24) {
+      P.merge12 = (a1 > 0 && a1 == a2 && d_x1 == d_x2 && ldx1 == ldx2) ? 1 : 0;
+      if (try_ws(P, PM, st, e)) {
+        if (e != cudaSuccess) {
+          set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+          return RG_ECUDA;
+        }
+        return launched();
+      }
+    }
+    RG_REQUIRE(gram_mode != 1 || gc <= (p <= 24 ? 32 : 16),
+               "rg_tall_f64: a %d-column Gram basis at p=%d needs the TMA ws path (16-byte aligned operands)",
+               gc, p);
     const int ncol_slabs = (P.zin ? (p + 7) / 8 : 0) + (a1 + 7) / 8 + (a2 + 7) / 8 +
                            (gram_mode == 1 ? (gc + 7) / 8 : 0);
     RG_REQUIRE(aligned && ncol_slabs <= kMaxSlabs && (P.a1 + P.a2) <= 128,

@@ -188,6 +188,11 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def _aligned16(t: torch.Tensor | None) -> bool:
+    """16-byte aligned base and an even leading dimension (what a tensor map needs)."""
+    return t is not None and t.data_ptr() % 16 == 0 and ld_of(t) % 2 == 0
+
+
 class Workspace:
     """Per-device scratch buffer; the leading 256 bytes hold the ticket
     counter of rg_tall's last-CTA reduction (zeroed once, re-armed by the
@@ -423,6 +428,9 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         return
     cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
     maxp, maxgc = (MAX_P_C, _c_limits(p, bool(terms))[0]) if cplx else (MAX_P, _r_limits(p)[0])
+    if (not cplx and 16 < p <= 24 and gram is not None and gram[0] == "basis" and not terms and r1 is None
+            and r2 is None and Z_out is None and _aligned16(Z_in) and _aligned16(gram[1])):
+        maxgc = MAX_GC  # a pure Gram of a 17..24-column block: the three-tile ws kernel takes 128 columns
     tcols = _c_limits(p)[1] if cplx else _r_limits(p)[1]
     terms = _split_terms(terms, tcols)
     r1 = _coef(r1) if r1 is not None else None

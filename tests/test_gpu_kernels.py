@@ -257,24 +257,28 @@ def test_tall_recycle_update_and_solution_shapes(cuda, n):
         return t
 
     for p, a1, a2, trsm, zin in ((20, 20, 88, False, False), (20, 20, 80, True, False), (8, 80, 20, False, True),
-                                 (16, 40, 60, True, True)):
+                                 (16, 40, 60, True, True), (20, 108, 0, False, False), (20, 20, 80, False, False),
+                                 (17, 108, 0, False, False), (24, 24, 88, False, False), (20, 88, 0, False, False)):
         X1, X2 = rng.standard_normal((n, a1)), rng.standard_normal((n, a2))
         S1, S2 = rng.standard_normal((a1, p)), rng.standard_normal((a2, p))
         Z = rng.standard_normal((n, p))
         R = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
         Zo = D.empty_block(n, p)
-        D.tall(blk(Z) if zin else None, Zo, [(blk(X1), small(S1), 1.0), (blk(X2), small(S2), -1.0)],
-               r1=small(R) if trsm else None, n=n, p=p)
+        terms = [(blk(X1), small(S1), 1.0)] + ([(blk(X2), small(S2), -1.0)] if a2 else [])
+        D.tall(blk(Z) if zin else None, Zo, terms, r1=small(R) if trsm else None, n=n, p=p)
         ref = (Z if zin else 0.0) + X1 @ S1 - X2 @ S2
         if trsm:
             ref = np.linalg.solve(R.T, ref.T).T
         assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12, (p, a1, a2, trsm, zin)
-    U = rng.standard_normal((n, 20))
-    for gc in (20, 32):
-        Gb = rng.standard_normal((n, gc))
-        G = D.small(gc, 20)
-        D.tall(blk(U), None, gram=("basis", blk(Gb), G))
-        assert _rel(G.cpu().numpy(), Gb.T @ U) <= 1e-12
+    # the cross Grams: C^T U and W^T U as one Gram against [C W] (three-tile
+    # ws kernel for p = 17..24, up to 128 basis columns)
+    for p in (20, 17, 24):
+        U = rng.standard_normal((n, p))
+        for gc in (20, 32, 108, 128):
+            Gb = rng.standard_normal((n, gc))
+            G = D.small(gc, p)
+            D.tall(blk(U), None, gram=("basis", blk(Gb), G))
+            assert _rel(G.cpu().numpy(), Gb.T @ U) <= 1e-12, (p, gc)
 
 
 def test_tall_empty_rows(cuda):

@@ -18,6 +18,7 @@ ap.add_argument("--store", action="store_true")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--trsm1", action="store_true")
 ap.add_argument("--trsm2", action="store_true")
+ap.add_argument("--noin", action="store_true", help="no Zin operand (z = the update terms only)")
 args = ap.parse_args()
 n, p = args.n, args.p
 g = torch.Generator(device="cuda"); g.manual_seed(0)
@@ -32,19 +33,19 @@ S2 = torch.randn(args.a2, p, device="cuda", dtype=torch.float64) if args.a2 else
 Zo = D.empty_block(n, p) if args.store else None
 terms = ([(X1, S1, -1.0)] if X1 is not None else []) + ([(X2, S2, -1.0)] if X2 is not None else [])
 gram = ("self", D.small(p, p)) if args.self else (("basis", Gb, D.small(args.gc, p)) if Gb is not None else None)
-cols = p + args.a1 + args.a2 + (args.gc if Gb is not None and not args.alias else 0) + (p if Zo is not None else 0)
+cols = (0 if args.noin else p) + args.a1 + args.a2 + (args.gc if Gb is not None and not args.alias else 0) + (p if Zo is not None else 0)
 if args.gc and args.a1 == args.gc and Gb is not None: pass
 R1 = torch.triu(torch.rand(p, p, device="cuda", dtype=torch.float64)) + 4 * torch.eye(p, device="cuda", dtype=torch.float64)
 r1 = R1 if (args.trsm1 or args.trsm2) else None
 r2 = R1 if args.trsm2 else None
 for _ in range(2):
-    D.tall(Z, Zo, terms, r1=r1, r2=r2, gram=gram)
+    D.tall(None if args.noin else Z, Zo, terms, r1=r1, r2=r2, gram=gram, n=n, p=p)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(args.reps):
-    D.tall(Z, Zo, terms, r1=r1, r2=r2, gram=gram)
+    D.tall(None if args.noin else Z, Zo, terms, r1=r1, r2=r2, gram=gram, n=n, p=p)
 e1.record(); torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStop()
 ms = e0.elapsed_time(e1) / args.reps
