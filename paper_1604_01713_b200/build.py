@@ -64,6 +64,11 @@ def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None =
             continue
         obj = objdir / (path.stem + ".o")
         objs.append(obj)
+        # an object newer than its source and every header is current (each
+        # objdir belongs to one flag set)
+        hdrs = [CSRC / h for h in HEADERS] + list(INCLUDE.glob("*.h")) + [pathlib.Path(__file__)]
+        if not force and obj.exists() and all(obj.stat().st_mtime > d.stat().st_mtime for d in [path, *hdrs]):
+            continue
         cmd = [nvcc, *NVCC_FLAGS, *(extra_flags or []), "-c", str(path), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")

@@ -1922,6 +1922,247 @@ static cudaError_t launch_v5(const TallParams& P, int64_t max_grid, cudaStream_t
     }                                                                                     \
     break;
 
+// ============================================================================
+// nr: narrow passes without update terms -- the CholQR2 solves (K_f: solve +
+// self-Gram, K_g: two solves + store), in-place scalings and column norms of
+// one n x p block (p <= 16).  Such a pass streams 8..16 columns only: through
+// whole 72-row ws stages (4.6 KB) or lane-per-row loads (v3) an SM cannot
+// keep enough bytes in flight (K_f ran at 0.52 of the copy peak on v3).
+// Here one producer thread keeps a ring of 256-row x PM-column boxes (16 KB
+// at p = 8, the tallest box a tensor map takes) full per CTA, two CTAs per
+// SM; the 8 consumer warps take 32 rows each, lane = row, pull their row
+// into registers and release the stage at once, so the ring never waits on
+// the solve, the store or the DMMA Gram.  Rows past n and columns past p
+// arrive as zeros (out-of-bounds fill).
+// ============================================================================
+
+#ifndef RG_TALL_NR
+#define RG_TALL_NR 1
+#endif
+constexpr int kNrRows = 256;
+constexpr int kNrWarps = 8;
+constexpr int kNrThreads = (kNrWarps + 1) * 32;
+constexpr int kNrMaxStages = 8;
+#ifndef RG_NR_CTAS
+#define RG_NR_CTAS 2
+#endif
+constexpr int kNrCtas = RG_NR_CTAS;  // CTAs per SM
+constexpr size_t kNrSmemMax = (kNrCtas == 2 ? 110 : 72) * 1024;
+
+template <int PM>
+__global__ void __launch_bounds__(kNrThreads, kNrCtas)
+    tall_nr_kernel(TallParams P, int stages, const __grid_constant__ CUtensorMap zmap) {
+  constexpr int NT = PM / 8;
+  constexpr int kStageWords = PM * kNrRows;
+  extern __shared__ __align__(128) double nr_smem[];
+  __shared__ __align__(8) uint64_t full[kNrMaxStages], empty[kNrMaxStages];
+  __shared__ bool s_last;
+  const int p = P.p;
+  double* stage0 = nr_smem;                                   // [stages][PM][256]
+  double* sR1 = stage0 + (size_t)stages * kStageWords;        // PM x PM row-major, reciprocal diagonal
+  double* sR2 = sR1 + PM * PM;
+  double* red = sR2 + PM * PM;                                // epilogue: max(NT*NT*64, kNrWarps*PM)
+  double* ztb = red + (NT * NT * 64 > kNrWarps * PM ? NT * NT * 64 : kNrWarps * PM);  // per warp [PM][36]
+
+  for (int e = threadIdx.x; e < PM * PM; e += kNrThreads) {
+    const int ii = e / PM, jj = e % PM;
+    const double id = ii == jj ? 1.0 : 0.0;
+    sR1[e] = (P.r1 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r1[ii + (int64_t)jj * p] : P.r1[ii + (int64_t)jj * p]) : id;
+    sR2[e] = (P.r2 && ii < p && jj < p) ? (ii == jj ? 1.0 / P.r2[ii + (int64_t)jj * p] : P.r2[ii + (int64_t)jj * p]) : id;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1u);
+      mbar_init(&empty[s], kNrWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mrow = lane >> 2, kq = lane & 3;
+  const int64_t nunits = (P.n + kNrRows - 1) / kNrRows;
+  const int64_t my_units =
+      (int64_t)blockIdx.x < nunits ? (nunits - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const bool gram_self = P.gmode == 2;
+
+  double acc[NT][NT][2], acb[NT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = acb[mt][nt][0] = acb[mt][nt][1] = 0.0;
+  double sq[PM];
+#pragma unroll
+  for (int c = 0; c < PM; ++c) sq[c] = 0.0;
+
+  if (warp == kNrWarps) {
+    // ---------------- producer: one thread, one tensor request per stage
+    if (lane == 0) {
+      int s = 0;
+      unsigned ph = 0;
+      for (int64_t it = 0; it < my_units; ++it) {
+        if (it >= stages) mbar_wait(&empty[s], ph ^ 1u);
+        const int row0 = (int)(((int64_t)blockIdx.x + it * gridDim.x) * kNrRows);
+        mbar_expect_tx(&full[s], (unsigned)(kStageWords * sizeof(double)));
+        tma_tile(stage0 + (size_t)s * kStageWords, &zmap, row0, &full[s]);
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers: lane = row (warp w: stage rows 32w .. 32w + 31)
+    double* zt = ztb + warp * PM * kSlabStride;
+    int s = 0;
+    unsigned ph = 0;
+    for (int64_t it = 0; it < my_units; ++it) {
+      mbar_wait(&full[s], ph);
+      const double* st = stage0 + (size_t)s * kStageWords + warp * 32 + lane;
+      double z[PM];
+#pragma unroll
+      for (int c = 0; c < PM; ++c) z[c] = st[c * kNrRows];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // the row is in registers: release the stage
+      if (++s == stages) {
+        s = 0;
+        ph ^= 1u;
+      }
+      const int64_t i = ((int64_t)blockIdx.x + it * gridDim.x) * kNrRows + warp * 32 + lane;
+      const bool valid = i < P.n;
+      if (P.r1) trsm_row<PM>(z, sR1, p);
+      if (P.r2) trsm_row<PM>(z, sR2, p);
+      if (!valid) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) z[c] = 0.0;
+      }
+      if (P.zout && valid) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c)
+          if (c < p) P.zout[i + (int64_t)c * P.ldzout] = z[c];
+      }
+      if (P.gmode == 3) {
+#pragma unroll
+        for (int c = 0; c < PM; ++c) sq[c] = fma(z[c], z[c], sq[c]);
+      }
+      if (gram_self) {
+        // DMMA Gram over these 32 rows (8 k-steps), fragments through the
+        // warp's padded tile
+#pragma unroll
+        for (int c = 0; c < PM; ++c) zt[c * kSlabStride + lane] = z[c];
+        __syncwarp();
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          double f[NT];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) f[nt] = zt[(nt * 8 + mrow) * kSlabStride + ks * 4 + kq];
+#pragma unroll
+          for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              // two accumulator chains (even / odd k-steps), summed at the end
+              if (ks & 1) dmma_nv(acb[mt][nt][0], acb[mt][nt][1], f[mt], f[nt]);
+              else dmma_nv(acc[mt][nt][0], acc[mt][nt][1], f[mt], f[nt]);
+            }
+        }
+        __syncwarp();
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        acc[mt][nt][0] += acb[mt][nt][0];
+        acc[mt][nt][1] += acb[mt][nt][1];
+      }
+  }
+
+  // ---------------- epilogue: deterministic reductions (as v3)
+  __syncthreads();
+  if (gram_self) {
+    for (int ww = 0; ww < kNrWarps; ++ww) {
+      if (warp == ww) {
+#pragma unroll
+        for (int mt = 0; mt < NT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int idx = ((mt * NT + nt) * 32 + lane) * 2 + v;
+              red[idx] = (ww == 0) ? acc[mt][nt][v] : red[idx] + acc[mt][nt][v];
+            }
+      }
+      __syncthreads();
+    }
+    const int ne = p * p;
+    for (int e = threadIdx.x; e < ne; e += kNrThreads) {
+      const int gg = e % p, c = e / p;
+      const int mt = gg >> 3, mr = gg & 7, nt = c >> 3, ncol = c & 7;
+      const int ln = mr * 4 + (ncol >> 1), v = ncol & 1;
+      P.part[(int64_t)blockIdx.x * ne + e] = red[((mt * NT + nt) * 32 + ln) * 2 + v];
+    }
+  } else if (P.gmode == 3) {
+    if (warp < kNrWarps) {
+#pragma unroll
+      for (int c = 0; c < PM; ++c) sq[c] = warp_sum(sq[c]);
+      if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < PM; ++c) red[warp * PM + c] = sq[c];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < p; c += kNrThreads) {
+      double sum = 0.0;
+      for (int ww = 0; ww < kNrWarps; ++ww) sum += red[ww * PM + c];
+      P.part[(int64_t)blockIdx.x * p + c] = sum;
+    }
+  }
+  if (P.gmode == 0) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(P.counter, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int ne = (P.gmode == 3) ? p : p * p;
+  for (int e = threadIdx.x; e < ne; e += kNrThreads) {
+    double sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
+    P.gout[e] = sum;
+  }
+  if (threadIdx.x == 0) *P.counter = 0u;
+}
+
+// false when the pass is not an nr shape or the tensor map cannot be encoded
+template <int PM>
+static bool try_nr(const TallParams& P, cudaStream_t st, cudaError_t& e) {
+  constexpr int NT = PM / 8;
+  CUtensorMap zmap;
+  memset(&zmap, 0, sizeof(zmap));
+  if (!encode_stage_map(&zmap, P.zin, P.ldzin, P.n, P.p, PM, kNrRows)) return false;
+  const size_t extra = ((size_t)2 * PM * PM + (size_t)std::max(NT * NT * 64, kNrWarps * PM) +
+                        (P.gmode == 2 ? (size_t)kNrWarps * PM * kSlabStride : 0)) * sizeof(double);
+  const size_t per_stage = (size_t)PM * kNrRows * sizeof(double);
+  int stages = kNrMaxStages;
+  while (stages >= 2 && (size_t)stages * per_stage + extra > kNrSmemMax) --stages;
+  if (stages < 2) return false;
+  auto k = tall_nr_kernel<PM>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNrSmemMax);
+    attr = true;
+  }
+  const int64_t nunits = (P.n + kNrRows - 1) / kNrRows;
+  int64_t g = (int64_t)sm_count() * kNrCtas;
+  if (nunits < g) g = nunits;
+  if (g < 1) g = 1;
+  k<<<(unsigned)g, kNrThreads, (size_t)stages * per_stage + extra, st>>>(P, stages, zmap);
+  e = cudaGetLastError();
+  return true;
+}
+
 static bool aligned16(const void* p, int64_t ld) {
   return p == nullptr || (((uintptr_t)p & 15u) == 0 && (ld & 1) == 0);
 }
@@ -2067,6 +2308,19 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
       return launched();
     }
     P.merge12 = 0;
+#if RG_TALL_NR
+    // one block in, no update terms (CholQR2 solves, scalings, norms): the
+    // 256-row TMA ring (cfg4: K_f 0.282 -> 0.217 ms, self-Gram 0.228 -> 0.173 ms; profiles/nr_r02.txt)
+    // (p = 9..16 measured slower than v3 / v6 there: 32 KB stages, 3 deep)
+    if (a1 + a2 == 0 && d_zin && gram_mode != 1 && (gram_mode != 0 || d_zout) && PM <= 8 &&
+        try_nr<8>(P, st, e)) {
+      if (e != cudaSuccess) {
+        set_error("rg_tall_f64: %s", cudaGetErrorString(e));
+        return RG_ECUDA;
+      }
+      return launched();
+    }
+#endif
     which = 6;
     if (a1 + a2 == 0) {
       if (gram_mode == 1)

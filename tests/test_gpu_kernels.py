@@ -152,6 +152,53 @@ def test_tall_trsm(cuda, p):
     assert _rel(D.to_numpy_block(Zo), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("n", [1, 255, 257, 1000, 70001])
+@pytest.mark.parametrize("p", [1, 3, 8, 13, 16])
+def test_tall_narrow_ring_passes(cuda, n, p):
+    """The one-block passes without update terms (the 256-row TMA ring,
+    tall_nr_kernel): CholQR2's K_f (solve + self-Gram) and K_g (two solves +
+    store, in place), plain self-Gram and column norms; ragged n, padding rows
+    and spare columns poisoned with NaN."""
+    D = _dev()
+    rng = np.random.default_rng(1000 * p + n)
+    Z = rng.standard_normal((n, p))
+    R1 = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
+    R2 = np.triu(rng.standard_normal((p, p))) + 4 * np.eye(p)
+    r1, r2 = torch.from_numpy(R1).to(cuda), torch.from_numpy(R2).to(cuda)
+
+    def poisoned(a):
+        store = torch.full((a.shape[1] + 3, D.round_ld(a.shape[0])), float("nan"), dtype=torch.float64, device=cuda)
+        v = store.t()[: a.shape[0], : a.shape[1]]
+        v.copy_(torch.from_numpy(np.asfortranarray(a).T).t())
+        return v
+
+    q1 = np.linalg.solve(R1.T, Z.T).T
+    q2 = np.linalg.solve(R2.T, q1.T).T
+    # K_f: solve + self-Gram, nothing stored
+    G = D.small(p, p)
+    D.tall(poisoned(Z), None, r1=r1, gram=("self", G))
+    assert _rel(G.cpu().numpy(), q1.T @ q1) <= 1e-12
+    # K_g: two solves, stored in place
+    Zd = poisoned(Z)
+    D.tall(Zd, Zd, r1=r1, r2=r2)
+    assert _rel(D.to_numpy_block(Zd), q2) <= 1e-12
+    # solve + store + norms of the result
+    Zo = poisoned(np.zeros((n, p)))
+    ss = torch.zeros(p, dtype=torch.float64, device=cuda)
+    D.tall(poisoned(Z), Zo, r1=r1, gram=("sumsq", ss))
+    assert _rel(D.to_numpy_block(Zo), q1) <= 1e-12
+    assert _rel(ss.cpu().numpy(), (q1 * q1).sum(axis=0)) <= 1e-12
+    # plain self-Gram and norms
+    D.tall(poisoned(Z), None, gram=("self", G))
+    assert _rel(G.cpu().numpy(), Z.T @ Z) <= 1e-12
+    D.tall(poisoned(Z), None, gram=("sumsq", ss))
+    assert _rel(ss.cpu().numpy(), (Z * Z).sum(axis=0)) <= 1e-12
+    # deterministic
+    G2 = D.small(p, p)
+    D.tall(poisoned(Z), None, gram=("self", G2))
+    assert torch.equal(G, G2)
+
+
 def test_tall_wide_terms_and_gram_split(cuda):
     """term lists longer than 2, basis wider than 128 columns, p > 16."""
     D = _dev()
@@ -466,7 +513,7 @@ def test_c_abi_cgs2_joint_schedule(cuda):
 
 
 @pytest.mark.parametrize("case", ["cfg1_2d", "cfg2_lap32", "cd3d_48", "banded_ragged"])
-@pytest.mark.parametrize("p", [1, 3, 8, 13])
+@pytest.mark.parametrize("p", [1, 3, 8, 13, 16, 20])
 def test_spmm_diagonal_layout_bitwise(cuda, case, p):
     """rg_spmm_dia_f64 (the stencil matrices' diagonal layout, TMA row
     windows) against rg_spmm_csr_f64 and the oracle: bitwise, including rows
