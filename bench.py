@@ -542,7 +542,9 @@ def solve_sequence_timed(grid, nsys, world, rank, dev):
                     "matvecs": rep.matvec_count, "converged": bool(rep.converged),
                     "rel_residual": float(rep.final_residual_norm / np.linalg.norm(rep.rhs_norms)),
                     "step_model_bytes": mb * world})
-    D.set_comm(None, None)
+    if world > 1:
+        D.set_comm(None, None)
+        comm.close()
     total_s = sum(r["s"] for r in per)
     total_steps = sum(r["block_steps"] for r in per)
     bsz = n_glob * P_BLOCK * 8

@@ -285,6 +285,50 @@ int rg_halo_pack(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const 
                  void* d_out, int64_t ldo, void* stream);
 
 /*
+ * Gram reduction over the row partition through peer memory (SURVEY.md §8e:
+ * "the (k+mp) x p Gram matrices are summed" across the GPUs; the reference is
+ * single-process -- its products arnoldi.py:172-180 are the global sums).
+ * One process per GPU on one node.  Each rank allocates an exchange buffer,
+ * passes its 64-byte CUDA IPC handle to the others (any host transport) and
+ * maps theirs; after rg_peer_set every Gram / norm pass of rg_tall_f64 /
+ * rg_tall_c128 (and so rg_cgs2_f64, rg_cholqr2_f64) finishes the sum over
+ * the ranks inside its own kernel: the CTA that sums the CTA partials stores
+ * its rank's values into every peer's slot (NVLink peer stores), publishes an
+ * epoch flag, waits for the peers' flags and adds the slots in rank order, so
+ * every rank holds the same bits.  No NCCL call and no extra launch.
+ *   rg_peer_buffer_bytes  size of one exchange buffer
+ *   rg_peer_alloc         allocate + zero the local buffer, return its handle
+ *   rg_peer_open/close    map / unmap a peer's buffer from its handle
+ *   rg_peer_free          release the local buffer
+ *   rg_peer_set           register the group (bufs[r] = rank r's buffer as
+ *                         mapped here; bufs[rank] = the local one); all ranks
+ *                         call it at the same point of their launch sequence;
+ *                         timeout_s bounds the in-kernel wait (<= 0: 20 s)
+ *   rg_peer_clear         back to single-process sums
+ *   rg_peer_active        0, or the registered world size
+ *   rg_peer_error         epoch at which a peer failed to arrive in time (0:
+ *                         none); synchronises the stream
+ *   rg_peer_allreduce_f64 in-place sum over the group of a small device
+ *                         buffer (<= 4096 doubles) no rg_tall pass produced
+ *   rg_peer_emulate_f64   tests: `world` ranks as one cooperative grid on one
+ *                         GPU over local exchange buffers (same device code)
+ * All reductions of a process go to one stream, in the same order on every
+ * rank.
+ */
+int64_t rg_peer_buffer_bytes(void);
+int rg_peer_alloc(void** d_buf, void* handle64);
+int rg_peer_open(const void* handle64, void** d_buf);
+int rg_peer_close(void* d_buf);
+int rg_peer_free(void* d_buf);
+int rg_peer_set(int32_t world, int32_t rank, void* const* bufs, double timeout_s);
+void rg_peer_clear(void);
+int32_t rg_peer_active(void);
+int rg_peer_error(uint32_t* epoch, void* stream);
+int rg_peer_allreduce_f64(double* d_buf, int64_t count, void* stream);
+int rg_peer_emulate_f64(int32_t world, int32_t ne, int32_t rounds, uint32_t epoch0, double* d_vals, void* d_buf,
+                        void* stream);
+
+/*
  * Launch accounting and per-launch device timing (no reference counterpart:
  * the reference times whole Python calls with perf_counter, bench.py:58-67).
  *   rg_launch_count    kernels launched by this library since load

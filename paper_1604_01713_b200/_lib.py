@@ -65,6 +65,17 @@ PROTOTYPES = {
     "rg_sptrsv_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i32,
                                      c_ptr,
                                      c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr]),
+    "rg_peer_buffer_bytes": (c_i64, []),
+    "rg_peer_alloc": (ctypes.c_int, [ctypes.POINTER(c_ptr), c_ptr]),
+    "rg_peer_open": (ctypes.c_int, [c_ptr, ctypes.POINTER(c_ptr)]),
+    "rg_peer_close": (ctypes.c_int, [c_ptr]),
+    "rg_peer_free": (ctypes.c_int, [c_ptr]),
+    "rg_peer_set": (ctypes.c_int, [c_i32, c_i32, ctypes.POINTER(c_ptr), c_dbl]),
+    "rg_peer_clear": (None, []),
+    "rg_peer_active": (c_i32, []),
+    "rg_peer_error": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint32), c_ptr]),
+    "rg_peer_allreduce_f64": (ctypes.c_int, [c_ptr, c_i64, c_ptr]),
+    "rg_peer_emulate_f64": (ctypes.c_int, [c_i32, c_i32, c_i32, ctypes.c_uint32, c_ptr, c_ptr, c_ptr]),
     "rg_launch_count": (c_i64, []),
     "rg_count_launches": (None, [c_i64]),
     "rg_profile_enable": (None, [c_i32]),

@@ -17,7 +17,7 @@ PKG = pathlib.Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "librgb200.so"
-SOURCES = ["rg_abi.cu", "rg_prof.cu", "rg_spmm.cu", "rg_tall.cu", "rg_qr.cu", "rg_steps.cu", "rg_cplx.cu", "rg_ilu.cu", "rg_halo.cu", "rg_dia.cu"]
+SOURCES = ["rg_abi.cu", "rg_prof.cu", "rg_spmm.cu", "rg_tall.cu", "rg_qr.cu", "rg_steps.cu", "rg_cplx.cu", "rg_ilu.cu", "rg_halo.cu", "rg_dia.cu", "rg_peer.cu"]
 HEADERS = ["rg_common.cuh"]
 INCLUDE = PKG.parent / "include"
 

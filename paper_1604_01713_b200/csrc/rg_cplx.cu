@@ -169,6 +169,7 @@ struct TallC {
   double2* gout;   // modes 1/2: gc x p complex; mode 3: p doubles (as double2 storage reused)
   double* part;
   unsigned* counter;
+  PeerComm comm;   // row-partitioned runs: Gout is summed over the ranks by the last CTA
 };
 
 constexpr int kTCWarps = 8;
@@ -426,6 +427,10 @@ __global__ void __launch_bounds__(kTCThreads, 1) tall_c128_kernel(TallC P) {
       P.gout[e] = make_double2(sr, si);
     }
   }
+  // row-partitioned: finish the sum over the ranks here (doubles: a complex sum is component-wise)
+  if (P.comm.world > 1)
+    peer_allreduce(P.comm, reinterpret_cast<double*>(P.gout), P.gmode == 3 ? p : 2 * P.gc * p, threadIdx.x,
+                   blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -936,6 +941,10 @@ __global__ void __launch_bounds__(kC6Threads, 1) tall_c6_kernel(TallC P, C6Plan 
       P.gout[e] = make_double2(sr, si);
     }
   }
+  // row-partitioned: finish the sum over the ranks here (doubles: a complex sum is component-wise)
+  if (P.comm.world > 1)
+    peer_allreduce(P.comm, reinterpret_cast<double*>(P.gout), P.gmode == 3 ? p : 2 * P.gc * p, threadIdx.x,
+                   blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -1065,6 +1074,7 @@ extern "C" int rg_tall_c128(int64_t n, int32_t p, const double* d_zin, int64_t l
   P.counter = (unsigned*)d_work;
   P.part = d_work ? (double*)((char*)d_work + 256) : nullptr;
   if (gram_mode == 0 && n == 0) return RG_OK;
+  P.comm = peer_comm_next(gram_mode != 0);
   cudaStream_t st0 = (cudaStream_t)stream;
   ProfScope prof(st0);
   auto launched = [&]() {

@@ -73,6 +73,7 @@ struct TallParams {
   unsigned int* counter;   // ticket
   int64_t ntiles;
   int merge12;             // v6: terms 1 and 2 share X -> one term with alpha1 S1 + alpha2 S2
+  PeerComm comm;           // row-partitioned runs: Gout is summed over the ranks by the last CTA
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -347,6 +348,8 @@ __global__ void __launch_bounds__(kV3Threads, (V3MinBlocks<PM, MTMAX>::value)) t
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
   }
+  // row-partitioned: finish the sum over the ranks here (rg_common.cuh)
+  if (P.comm.world > 1) peer_allreduce(P.comm, P.gout, ne, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -620,6 +623,8 @@ __global__ void __launch_bounds__(kV5Threads, V5MinBlocks<MTMAX>::value) tall_v5
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
   }
+  // row-partitioned: finish the sum over the ranks here (rg_common.cuh)
+  if (P.comm.world > 1) peer_allreduce(P.comm, P.gout, ne, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -1045,6 +1050,8 @@ __global__ void __launch_bounds__(W6 * 32, PM > 16 ? 1 : 2) tall_v6_kernel(TallP
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
   }
+  // row-partitioned: finish the sum over the ranks here (rg_common.cuh)
+  if (P.comm.world > 1) peer_allreduce(P.comm, P.gout, ne, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -1532,6 +1539,8 @@ __global__ void __launch_bounds__((WsGeom<CW, TMA>::kThreads), (WsGeom<CW, TMA>:
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
   }
+  // row-partitioned: finish the sum over the ranks here (rg_common.cuh)
+  if (P.comm.world > 1) peer_allreduce(P.comm, P.gout, ne, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -2132,6 +2141,8 @@ __global__ void __launch_bounds__(kNrThreads, kNrCtas)
     for (unsigned b = 0; b < gridDim.x; ++b) sum += __ldcg(P.part + (int64_t)b * ne + e);
     P.gout[e] = sum;
   }
+  // row-partitioned: finish the sum over the ranks here (rg_common.cuh)
+  if (P.comm.world > 1) peer_allreduce(P.comm, P.gout, ne, threadIdx.x, blockDim.x);
   if (threadIdx.x == 0) *P.counter = 0u;
 }
 
@@ -2231,6 +2242,7 @@ extern "C" int rg_tall_f64(int64_t n, int32_t p, const double* d_zin, int64_t ld
   P.ntiles = (n + kTallThreads - 1) / kTallThreads;
   P.merge12 = 0;
   if (gram_mode == 0 && P.ntiles == 0) return RG_OK;
+  P.comm = peer_comm_next(gram_mode != 0);
   ProfScope prof((cudaStream_t)stream);
   auto launched = [&]() {
     // algorithmic bytes: every streamed operand column once (a Gram basis

@@ -375,8 +375,8 @@ def _tall_call(n, p, zin, zout, t1, t2, r1, r2, gmode, gb, gout, cplx=False):
     Workspace.check(f"rg_tall n={n} p={p} a={a1}+{a2} gmode={gmode} gc={gc} cplx={cplx}")
     if gout_k is not gout:
         gout.copy_(gout_k)
-    if gmode and _COMM is not None:
-        _COMM.allreduce_(gout)
+    if gmode and _COMM is not None and not _COMM.peer_active:
+        _COMM.allreduce_(gout)  # (peer group: the kernel's last CTA summed over the ranks)
 
 
 def _dense_f(t: torch.Tensor) -> bool:
@@ -425,6 +425,10 @@ def tall(Z_in: torch.Tensor | None, Z_out: torch.Tensor | None, terms=(), r1=Non
         p = (Z_in if Z_in is not None else Z_out).shape[1]
     if n == 0 and gram is not None:
         _zero_gram(gram)
+        if _COMM is not None and _COMM.peer_active:
+            # every rank must launch the same sequence of reducing passes
+            raise _lib.KernelError("row partition with an empty rank: the in-kernel Gram reduction needs rows on "
+                                   "every rank")
         return
     cplx = any(t is not None and t.dtype == torch.complex128 for t in (Z_in, Z_out))
     maxp, maxgc = (MAX_P_C, _c_limits(p, bool(terms))[0]) if cplx else (MAX_P, _r_limits(p)[0])
@@ -551,9 +555,10 @@ def max_p(t: torch.Tensor) -> int:
 
 def fused_ok() -> bool:
     """The C orchestrators (rg_cgs2_f64 / rg_cholqr2_f64) replace the Python
-    pass chain on one GPU; row-partitioned runs need the Gram allreduce
-    between passes."""
-    return _COMM is None
+    pass chain on one GPU, and on a row partition whose Gram passes sum over
+    the ranks in-kernel (distributed.PeerGroup); with NCCL allreduces between
+    the passes the Python chain runs."""
+    return _COMM is None or _COMM.peer_active
 
 
 def cgs2(Z: torch.Tensor, C, W: torch.Tensor, coef: torch.Tensor, G1, joint: bool = False) -> None:

@@ -22,6 +22,12 @@ scaling layer:
 * ``CommContext``    the sum-allreduce applied to every Gram / norm that
                      rg_tall produces (device.set_comm); the (k+mp) x p
                      Grams are a few KB, i.e. latency-bound.
+* ``PeerGroup``      the ranks of one node map each other's exchange buffers
+                     (CUDA IPC over NVLink); the Gram passes then finish the
+                     sum over the ranks inside their own kernels
+                     (rg_common.cuh peer_allreduce): no NCCL call per Gram,
+                     and the C orchestrators (rg_cgs2_f64 / rg_cholqr2_f64)
+                     run unchanged on a row partition.
 
 Host-side small problems (progressive LS, harmonic Ritz) are replicated on
 every rank from bitwise-identical allreduced inputs.  Seeded random vectors
@@ -166,16 +172,149 @@ def _exchange_recv_lists(part: RowPartition, recv_lists: dict) -> dict:
 # ---------------------------------------------------------------------------
 
 
+def peer_eligible(infos, max_world: int = 8):
+    """Can these ranks reduce through peer memory?  ``infos`` is every
+    rank's (hostname, CUDA device index or None).  Returns (ok, reason):
+    one node, one distinct GPU per rank, 2..max_world ranks."""
+    world = len(infos)
+    if world < 2:
+        return False, "single rank"
+    if world > max_world:
+        return False, f"{world} ranks > {max_world}"
+    hosts = {h for h, _ in infos}
+    if len(hosts) != 1:
+        return False, f"ranks span {len(hosts)} hosts"
+    devs = [d for _, d in infos]
+    if any(d is None for d in devs):
+        return False, "a rank has no CUDA device"
+    if len(set(devs)) != world:
+        return False, "ranks share a GPU (kernels of different ranks must run concurrently)"
+    return True, "ok"
+
+
+class PeerGroup:
+    """Exchange buffers of the node's ranks, mapped into each other with
+    CUDA IPC, registered with librgb200 (rg_peer_set): from then on every
+    Gram / norm pass sums over the ranks inside its own kernel.  ``create``
+    returns None (with the reason on stderr) when the ranks are not eligible
+    or the self-test fails; the NCCL allreduce then stays in charge."""
+
+    SELFTEST_TIMEOUT_S = 5.0
+
+    def __init__(self, comm, local, mapped, timeout_s):
+        self.comm, self.local, self.mapped, self.timeout_s = comm, local, mapped, timeout_s
+
+    @classmethod
+    def create(cls, comm: "CommContext", timeout_s: float = 20.0):
+        import ctypes
+        import os
+        import socket
+        import sys
+
+        if os.environ.get("RG_PEER_GRAM", "1") == "0" or not comm.nccl or not torch.cuda.is_available():
+            return None
+        infos = [None] * comm.world
+        dist.all_gather_object(infos, (socket.gethostname(), torch.cuda.current_device()), group=comm.group)
+        ok, why = peer_eligible(infos)
+        if not ok:
+            if comm.rank == 0 and comm.world > 1:
+                print(f"[rgb200] peer-memory Gram reduction off: {why}", file=sys.stderr)
+            return None
+        L = _dev.lib()
+        buf, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        _lib.check(L.rg_peer_alloc(ctypes.byref(buf), handle), "peer alloc")
+        handles = [None] * comm.world
+        dist.all_gather_object(handles, handle.raw, group=comm.group)
+        ptrs, mapped, failed = [], [], False
+        for r, h in enumerate(handles):
+            if r == comm.rank:
+                ptrs.append(buf.value)
+                continue
+            q = ctypes.c_void_p()
+            if L.rg_peer_open(h, ctypes.byref(q)) != _lib.RG_OK:
+                failed = True
+                break
+            ptrs.append(q.value)
+            mapped.append(q.value)
+        # all ranks agree on the outcome before anything is registered
+        flag = torch.tensor([1 if failed else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=comm.group)
+        self = cls(comm, buf.value, mapped, timeout_s)
+        if int(flag.item()):
+            self._release()
+            if comm.rank == 0:
+                print("[rgb200] peer-memory Gram reduction off: cudaIpcOpenMemHandle failed", file=sys.stderr)
+            return None
+        arr = (ctypes.c_void_p * comm.world)(*ptrs)
+        dist.barrier(group=comm.group)
+        _lib.check(L.rg_peer_set(comm.world, comm.rank, arr, cls.SELFTEST_TIMEOUT_S), "peer set")
+        # self-test: one reduction of known values, bounded wait
+        t = torch.full((8,), float(comm.rank + 1), dtype=torch.float64, device="cuda")
+        _lib.check(L.rg_peer_allreduce_f64(t.data_ptr(), 8, _dev.stream_ptr()), "peer allreduce")
+        bad = self.error_epoch() != 0 or not bool((t == comm.world * (comm.world + 1) / 2).all().item())
+        flag = torch.tensor([1 if bad else 0], device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=comm.group)
+        if int(flag.item()):
+            L.rg_peer_clear()
+            self._release()
+            if comm.rank == 0:
+                print("[rgb200] peer-memory Gram reduction off: self-test failed", file=sys.stderr)
+            return None
+        dist.barrier(group=comm.group)
+        _lib.check(L.rg_peer_set(comm.world, comm.rank, arr, timeout_s), "peer set")
+        return self
+
+    def error_epoch(self) -> int:
+        import ctypes
+
+        e = ctypes.c_uint32(0)
+        _lib.check(_dev.lib().rg_peer_error(ctypes.byref(e), _dev.stream_ptr()), "peer error")
+        return int(e.value)
+
+    def check(self) -> None:
+        e = self.error_epoch()
+        if e:
+            raise _lib.KernelError(f"peer-memory Gram reduction {e}: a rank did not arrive within {self.timeout_s} s")
+
+    def _release(self):
+        L = _dev.lib()
+        for q in self.mapped:
+            L.rg_peer_close(q)
+        self.mapped = []
+        if self.local:
+            L.rg_peer_free(self.local)
+            self.local = None
+
+    def close(self):
+        torch.cuda.synchronize()
+        dist.barrier(group=self.comm.group)
+        _dev.lib().rg_peer_clear()
+        self._release()
+
+
 class CommContext:
     """Sum-allreduce of Grams and point-to-point halo transport over a
     torch.distributed group.  NCCL moves CUDA buffers directly (NVLink);
-    other backends (gloo, used by the CPU tests) stage through host memory."""
+    other backends (gloo, used by the CPU tests) stage through host memory.
+    With NCCL on one node the Gram sums move into the producing kernels
+    (``PeerGroup``); ``allreduce_`` then serves only the buffers no rg_tall
+    pass produced."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, peer: bool = True):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.nccl = dist.get_backend(group) == "nccl"
+        self.peer = PeerGroup.create(self) if (peer and self.world > 1) else None
+
+    @property
+    def peer_active(self) -> bool:
+        return self.peer is not None
+
+    def close(self):
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
 
     def allreduce_(self, t: torch.Tensor) -> torch.Tensor:
         if self.world == 1:
@@ -361,4 +500,7 @@ def setup(A, group=None, align: int = 1, device=None):
 
 
 def teardown():
+    comm = _dev.get_comm()
     _dev.set_comm(None, None)
+    if comm is not None:
+        comm.close()

@@ -158,3 +158,42 @@ def _dist_tsqr_worker(rank, world):
 
 def test_distributed_tsqr_combine():
     _run(2, _dist_tsqr_worker)
+
+
+# ---------------------------------------------------------------- peer-memory Gram reduction (host logic)
+
+
+def test_peer_eligibility_rules():
+    from paper_1604_01713_b200.distributed import peer_eligible
+
+    assert peer_eligible([("a", 0), ("a", 1)]) == (True, "ok")
+    assert peer_eligible([("a", r) for r in range(8)])[0]
+    assert not peer_eligible([("a", 0)])[0]                          # nothing to reduce
+    assert not peer_eligible([("a", r) for r in range(9)])[0]        # more ranks than slots
+    assert not peer_eligible([("a", 0), ("b", 1)])[0]                # two nodes: no IPC mapping
+    assert not peer_eligible([("a", 0), ("a", 0)])[0]                # ranks sharing a GPU would wait on each other
+    assert not peer_eligible([("a", 0), ("a", None)])[0]
+
+
+def _peer_off_worker(rank, world):
+    """gloo ranks never register a peer group: the Gram sums stay on the
+    group's allreduce and the fused C orchestrators stay off."""
+    from paper_1604_01713_b200 import device as D
+    from paper_1604_01713_b200.distributed import CommContext, RowPartition
+
+    comm = CommContext()
+    assert comm.peer is None and not comm.peer_active
+    D.set_comm(comm, RowPartition.even(100, world, rank))
+    try:
+        assert not D.fused_ok()
+        t = torch.full((4,), float(rank + 1), dtype=torch.float64)
+        comm.allreduce_(t)
+        assert torch.equal(t, torch.full((4,), 3.0, dtype=torch.float64))
+    finally:
+        D.set_comm(None, None)
+        comm.close()
+    assert D.fused_ok()
+
+
+def test_peer_group_off_under_gloo():
+    _run(2, _peer_off_worker)
