@@ -285,6 +285,27 @@ int rg_halo_pack(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const 
                  void* d_out, int64_t ldo, void* stream);
 
 /*
+ * The same exchange without a transport library, for the ranks of one node:
+ *   rg_halo_push  the gather of rg_halo_pack stored straight into the peer's
+ *                 ghost block (d_peer_out: a CUDA IPC mapping, rg_ipc_alloc /
+ *                 rg_peer_open; NVLink peer stores), then flag = epoch on the
+ *                 peer (d_peer_flag, mapped) once every CTA's stores are
+ *                 fenced (d_ticket: a zeroed local counter); k = 0 only
+ *                 publishes the flag
+ *   rg_halo_wait  one small kernel ahead of the boundary rows: waits until
+ *                 d_flags[peers[i]] == epoch for every listed peer (host
+ *                 array, <= 8), at most timeout_s, else *d_err = epoch
+ * Ghost blocks alternate between two buffers with the epoch's parity, and
+ * every pair of neighbours signals both ways each epoch, so a rank can be at
+ * most one product ahead of a neighbour and never overwrites rows being read.
+ */
+int rg_halo_push(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const void* d_z, int64_t ldz,
+                 void* d_peer_out, int64_t ldo, uint32_t* d_peer_flag, uint32_t epoch, uint32_t* d_ticket,
+                 void* stream);
+int rg_halo_wait(const uint32_t* d_flags, const int32_t* peers, int32_t npeers, uint32_t epoch, double timeout_s,
+                 uint32_t* d_err, void* stream);
+
+/*
  * Gram reduction over the row partition through peer memory (SURVEY.md §8e:
  * "the (k+mp) x p Gram matrices are summed" across the GPUs; the reference is
  * single-process -- its products arnoldi.py:172-180 are the global sums).
@@ -316,6 +337,7 @@ int rg_halo_pack(int64_t k, int32_t p, int32_t esz, const int32_t* d_idx, const 
  * rank.
  */
 int64_t rg_peer_buffer_bytes(void);
+int rg_ipc_alloc(int64_t bytes, void** d_buf, void* handle64); /* any size (ghost blocks, halo flags) */
 int rg_peer_alloc(void** d_buf, void* handle64);
 int rg_peer_open(const void* handle64, void** d_buf);
 int rg_peer_close(void* d_buf);

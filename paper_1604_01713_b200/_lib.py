@@ -65,6 +65,10 @@ PROTOTYPES = {
     "rg_sptrsv_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_i32, c_i32,
                                      c_ptr,
                                      c_i64, c_ptr, c_i64, c_ptr, c_i64, c_i32, c_ptr]),
+    "rg_halo_push": (ctypes.c_int, [c_i64, c_i32, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, ctypes.c_uint32,
+                                    c_ptr, c_ptr]),
+    "rg_halo_wait": (ctypes.c_int, [c_ptr, ctypes.POINTER(c_i32), c_i32, ctypes.c_uint32, c_dbl, c_ptr, c_ptr]),
+    "rg_ipc_alloc": (ctypes.c_int, [c_i64, ctypes.POINTER(c_ptr), c_ptr]),
     "rg_peer_buffer_bytes": (c_i64, []),
     "rg_peer_alloc": (ctypes.c_int, [ctypes.POINTER(c_ptr), c_ptr]),
     "rg_peer_open": (ctypes.c_int, [c_ptr, ctypes.POINTER(c_ptr)]),

@@ -55,18 +55,23 @@ extern "C" int64_t rg_peer_buffer_bytes(void) { return (int64_t)kPeerBytes; }
 
 // a zeroed exchange buffer of rg_peer_buffer_bytes() bytes and its IPC handle
 // (64 bytes) for the other ranks of the node
-extern "C" int rg_peer_alloc(void** d_buf, void* handle64) {
+extern "C" int rg_peer_alloc(void** d_buf, void* handle64) { return rg_ipc_alloc((int64_t)kPeerBytes, d_buf, handle64); }
+
+// a zeroed device allocation of its own (cudaMalloc, not a sub-block of a
+// pool: an IPC handle names a whole allocation) and its 64-byte handle;
+// mapped by peers with rg_peer_open, released with rg_peer_free
+extern "C" int rg_ipc_alloc(int64_t bytes, void** d_buf, void* handle64) {
   clear_error();
-  RG_REQUIRE(d_buf && handle64, "rg_peer_alloc: null argument");
+  RG_REQUIRE(d_buf && handle64 && bytes > 0, "rg_ipc_alloc: bad arguments");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, kPeerBytes);
-  if (e == cudaSuccess) e = cudaMemset(p, 0, kPeerBytes);
+  cudaError_t e = cudaMalloc(&p, (size_t)bytes);
+  if (e == cudaSuccess) e = cudaMemset(p, 0, (size_t)bytes);
   cudaIpcMemHandle_t h;
   if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
   if (e != cudaSuccess) {
     if (p) cudaFree(p);
-    set_error("rg_peer_alloc: %s", cudaGetErrorString(e));
+    set_error("rg_ipc_alloc: %s", cudaGetErrorString(e));
     return RG_ECUDA;
   }
   memcpy(handle64, &h, 64);
