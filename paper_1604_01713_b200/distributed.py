@@ -203,6 +203,7 @@ class PeerGroup:
 
     def __init__(self, comm, local, mapped, timeout_s):
         self.comm, self.local, self.mapped, self.timeout_s = comm, local, mapped, timeout_s
+        self.halos = []  # HaloPeer objects of the operators built on this group
 
     @classmethod
     def create(cls, comm: "CommContext", timeout_s: float = 20.0):
@@ -275,9 +276,14 @@ class PeerGroup:
         e = self.error_epoch()
         if e:
             raise _lib.KernelError(f"peer-memory Gram reduction {e}: a rank did not arrive within {self.timeout_s} s")
+        for h in self.halos:
+            h.check()
 
     def _release(self):
         L = _dev.lib()
+        for h in self.halos:
+            h.release()
+        self.halos = []
         for q in self.mapped:
             L.rg_peer_close(q)
         self.mapped = []
@@ -290,6 +296,157 @@ class PeerGroup:
         dist.barrier(group=self.comm.group)
         _dev.lib().rg_peer_clear()
         self._release()
+
+
+class _DevView:
+    """A raw device allocation as a CUDA-array-interface object."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap(ptr: int, shape, dtype, device) -> torch.Tensor:
+    typestr = {torch.float64: "<f8", torch.complex128: "<c16", torch.int32: "<i4"}[dtype]
+    return torch.as_tensor(_DevView(ptr, shape, typestr), device=device)
+
+
+class _GhostBlocks:
+    """Two ghost blocks (epoch parity) of one (p, dtype) in an IPC
+    allocation, and the neighbours' mappings of theirs."""
+
+    def __init__(self, local_ptr, tensor, peer_ptr):
+        self.local_ptr, self.local, self.peer_ptr = local_ptr, tensor, peer_ptr  # tensor: (2, p, n_ghost)
+
+
+class HaloPeer:
+    """Halo exchange of one DistCsr without a transport library: each rank
+    stores the rows a neighbour needs straight into that neighbour's ghost
+    block (rg_halo_push: NVLink peer stores + an epoch flag) and waits for its
+    own neighbours' flags ahead of the boundary rows (rg_halo_wait).  Ghost
+    blocks alternate with the epoch's parity and every pair of neighbours
+    signals both ways, so a rank is never more than one product ahead of a
+    neighbour.  All products of the operator go to one stream, in the same
+    order on every rank.
+
+    flags (uint32, one IPC allocation per rank): [par * 8 + src] epochs,
+    [16] push ticket, [17] error word."""
+
+    FLAG_WORDS = 64
+    TIMEOUT_S = 20.0
+
+    def __init__(self, rank, peers, dst, flags_local, flags_peer, n_ghost, device, opener=None, mapped=None):
+        self.rank, self.peers, self.dst = rank, list(peers), dict(dst)
+        self.flags_local, self.flags_peer = flags_local, dict(flags_peer)
+        self.n_ghost, self.device = n_ghost, device
+        self.epoch = 0
+        self._ghosts = {}
+        self._opener = opener      # (p, dtype, nbytes) -> _GhostBlocks (collective); tests inject pointers
+        self._mapped = list(mapped or [])
+        self._owned = [flags_local] if opener is not None else []
+        import ctypes
+
+        self._peer_arr = (ctypes.c_int32 * max(len(self.peers), 1))(*self.peers)
+
+    @classmethod
+    def create(cls, plan: "HaloPlan", comm: "CommContext", device):
+        """Collective over the group: exchange the flag handles, each rank's
+        ghost layout (who lands where) and neighbour sets."""
+        import ctypes
+
+        L = _dev.lib()
+        buf, handle = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+        _lib.check(L.rg_ipc_alloc(4 * cls.FLAG_WORDS, ctypes.byref(buf), handle), "ipc alloc")
+        mine = {"recv": dict(plan.recv_ranges), "send": sorted(plan.send_rows), "n_ghost": plan.n_ghost,
+                "flags": handle.raw}
+        infos = [None] * comm.world
+        dist.all_gather_object(infos, mine, group=comm.group)
+        me = comm.rank
+        peers = neighbours(infos, me)
+        dst = {q: (infos[q]["recv"][me][0], max(infos[q]["n_ghost"], 1)) for q in peers if me in infos[q]["recv"]}
+        flags_peer, mapped = {}, []
+        for q in peers:
+            ptr = ctypes.c_void_p()
+            _lib.check(L.rg_peer_open(infos[q]["flags"], ctypes.byref(ptr)), "peer open")
+            flags_peer[q] = ptr.value
+            mapped.append(ptr.value)
+
+        def opener(p, dtype, nbytes):
+            b, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+            _lib.check(L.rg_ipc_alloc(nbytes, ctypes.byref(b), h), "ipc alloc")
+            hs = [None] * comm.world
+            dist.all_gather_object(hs, h.raw, group=comm.group)
+            peer_ptr = {}
+            for q in peers:
+                ptr = ctypes.c_void_p()
+                _lib.check(L.rg_peer_open(hs[q], ctypes.byref(ptr)), "peer open")
+                peer_ptr[q] = ptr.value
+                self._mapped.append(ptr.value)
+            self._owned.append(b.value)
+            dist.barrier(group=comm.group)
+            return _GhostBlocks(b.value, _wrap(b.value, (2, p, max(plan.n_ghost, 1)), dtype, device), peer_ptr)
+
+        self = cls(me, peers, dst, buf.value, flags_peer, plan.n_ghost, device, opener, mapped)
+        dist.barrier(group=comm.group)
+        return self
+
+    def ghost(self, p: int, dtype) -> _GhostBlocks:
+        key = (p, dtype)
+        if key not in self._ghosts:
+            esz = 16 if dtype == torch.complex128 else 8
+            self._ghosts[key] = self._opener(p, dtype, 2 * p * max(self.n_ghost, 1) * esz)
+        return self._ghosts[key]
+
+    def push_all(self, Z: torch.Tensor, send_idx: dict, gb: _GhostBlocks) -> int:
+        """Next epoch: store this rank's rows into every neighbour's ghost
+        block of that parity and publish the flag (k = 0: the flag only)."""
+        L, st = _dev.lib(), _dev.stream_ptr()
+        self.epoch += 1
+        par = self.epoch & 1
+        p = Z.shape[1]
+        esz = 16 if Z.dtype == torch.complex128 else 8
+        for q in self.peers:
+            idx = send_idx.get(q)
+            k = 0 if idx is None else idx.numel()
+            s0, ldq = self.dst.get(q, (0, 1))
+            out = gb.peer_ptr[q] + (par * p * ldq + s0) * esz if k else None
+            _lib.check(L.rg_halo_push(k, p, esz, idx.data_ptr() if k else None, Z.data_ptr(), _dev.ld_of(Z), out, ldq,
+                                      self.flags_peer[q] + 4 * (par * 8 + self.rank), self.epoch,
+                                      self.flags_local + 4 * 16, st), "halo push")
+        return par
+
+    def wait_all(self) -> None:
+        if not self.peers:
+            return
+        par = self.epoch & 1
+        _lib.check(_dev.lib().rg_halo_wait(self.flags_local + 4 * (par * 8), self._peer_arr, len(self.peers),
+                                           self.epoch, self.TIMEOUT_S, self.flags_local + 4 * 17,
+                                           _dev.stream_ptr()), "halo wait")
+
+    def check(self) -> None:
+        e = int(_wrap(self.flags_local, (self.FLAG_WORDS,), torch.int32, self.device)[17].item())
+        if e:
+            raise _lib.KernelError(f"halo exchange {e}: a neighbour's rows did not arrive within {self.TIMEOUT_S} s")
+
+    def release(self) -> None:
+        L = _dev.lib()
+        for q in self._mapped:
+            L.rg_peer_close(q)
+        for b in self._owned:
+            L.rg_peer_free(b)
+        self._mapped, self._owned, self._ghosts = [], [], {}
+
+
+def neighbours(infos, me: int):
+    """Ranks this rank exchanges flags with: everyone it sends rows to or
+    receives rows from, made symmetric (q lists me => I list q), so that each
+    pair signals both ways every product."""
+    mine = set(infos[me]["send"]) | set(infos[me]["recv"])
+    for q, inf in enumerate(infos):
+        if q != me and (me in inf["send"] or me in inf["recv"]):
+            mine.add(q)
+    mine.discard(me)
+    return sorted(int(q) for q in mine)
 
 
 class CommContext:
@@ -405,6 +562,11 @@ class DistCsr:
                           for q, v in plan.send_rows.items()}
         self._ghost = {}
         self._sendbuf = {}
+        # ranks of one node under NCCL: neighbours store into each other's ghost blocks
+        self._halo_peer = None
+        if local_spmm is None and comm is not None and getattr(comm, "peer_active", False):
+            self._halo_peer = HaloPeer.create(plan, comm, dev)
+            comm.peer.halos.append(self._halo_peer)
 
     def _ghost_block(self, p, dtype):
         key = (p, dtype)
@@ -433,6 +595,22 @@ class DistCsr:
     def apply_into(self, Z: torch.Tensor, out: torch.Tensor) -> None:
         plan = self.plan
         p = Z.shape[1]
+        i0, i1 = plan.interior
+        if self._halo_peer is not None and Z.is_cuda:
+            # peer stores into the neighbours' ghost blocks, the interior rows
+            # while they travel, one wait kernel, then the boundary rows
+            hp = self._halo_peer
+            gb = hp.ghost(p, Z.dtype)
+            par = hp.push_all(Z, self._send_idx, gb)
+            if i1 > i0:
+                self._spmm(Z, out, i0, i1, None)
+            hp.wait_all()
+            Xg = gb.local[par].t()[: plan.n_ghost] if plan.n_ghost else None
+            if i0 > 0:
+                self._spmm(Z, out, 0, i0, Xg)
+            if i1 < self.n_rows:
+                self._spmm(Z, out, max(i1, i0), self.n_rows, Xg)
+            return
         G = self._ghost_block(p, Z.dtype)
         # pack the rows each peer needs (one kernel per peer); every column of
         # a send buffer is one message, received straight into the matching
@@ -446,7 +624,6 @@ class DistCsr:
             for c in range(p):
                 recvs[(q, c)] = G[c, s0:s1]
         works, staged = self.comm.exchange(sends, recvs) if self.comm is not None else ([], [])
-        i0, i1 = plan.interior
         # interior rows need no ghost column: overlap them with the exchange
         if i1 > i0:
             self._spmm(Z, out, i0, i1, None)

@@ -197,3 +197,18 @@ def _peer_off_worker(rank, world):
 
 def test_peer_group_off_under_gloo():
     _run(2, _peer_off_worker)
+
+
+def test_halo_neighbours_are_symmetric():
+    """Each pair of ranks that exchanges rows in either direction signals
+    both ways (the flow control of the peer-store halo exchange)."""
+    from paper_1604_01713_b200.distributed import neighbours
+
+    # rank 0 sends to 1 only; rank 2 receives from 1 only; rank 3 isolated
+    infos = [{"send": [1], "recv": {}}, {"send": [2], "recv": {0: (0, 4)}}, {"send": [], "recv": {1: (0, 3)}},
+             {"send": [], "recv": {}}]
+    nb = [neighbours(infos, r) for r in range(4)]
+    assert nb == [[1], [0, 2], [1], []]
+    for r, qs in enumerate(nb):
+        for q in qs:
+            assert r in nb[q]

@@ -213,3 +213,72 @@ def test_gram_passes_reduce_over_ranks_in_kernel(cuda, shape):
             assert np.array_equal(got, (0.0 + sent) + peer_vals[epoch - 1])  # rank-order sum, bitwise
     finally:
         fake.close()
+
+
+@pytest.mark.parametrize("p", [1, 8])
+@pytest.mark.parametrize("me", [0, 1, 2])
+def test_halo_push_with_prearmed_neighbours(cuda, me, p):
+    """The transport-free halo exchange of DistCsr (rg_halo_push /
+    rg_halo_wait) for one rank of a 3-rank partition: the neighbours' rows and
+    flags are written into this rank's ghost blocks before each product, so no
+    kernel waits on another.  The product equals the single-process SpMM
+    bitwise; the stand-ins for the neighbours' ghost blocks receive this rank's
+    boundary rows at the right offsets with the epoch flag, on both parities."""
+    import oracle
+    from paper_1604_01713_b200 import device as D, problems
+    from paper_1604_01713_b200 import distributed as DI
+
+    world, grid = 3, 9
+    A = problems.conv_diff_3d(grid, 20.0)
+    rng = np.random.default_rng(11 + me)
+    plans, lists = [], {}
+    parts = [DI.RowPartition.even(A.n_rows, world, r, align=grid * grid) for r in range(world)]
+    blocks = [DI.csr_row_block(A.row_ptr, A.col_idx, A.values, pt.r0, pt.r1) for pt in parts]
+    # first pass collects every rank's recv lists, second builds the plans with a local "exchange"
+    for r in range(world):
+        DI.HaloPlan.from_local_rows(parts[r], *blocks[r], exchange=lambda part, rl: lists.setdefault(part.rank, rl) and {})
+    ex = lambda part, rl: {q: lists[q][part.rank] for q in range(world) if q != part.rank and part.rank in lists[q]}  # noqa: E731
+    plans = [DI.HaloPlan.from_local_rows(parts[r], *blocks[r], exchange=ex) for r in range(world)]
+    plan, part = plans[me], parts[me]
+    infos = [{"send": sorted(pl.send_rows), "recv": dict(pl.recv_ranges)} for pl in plans]
+    peers = DI.neighbours(infos, me)
+    assert peers == {0: [1], 1: [0, 2], 2: [1]}[me]
+
+    flags_local = torch.zeros(64, dtype=torch.int32, device=cuda)
+    flags_peer_t = {q: torch.zeros(64, dtype=torch.int32, device=cuda) for q in peers}
+    ghost_local = torch.zeros((2, p, max(plan.n_ghost, 1)), dtype=torch.float64, device=cuda)
+    ghost_peer_t = {q: torch.full((2, p, max(plans[q].n_ghost, 1)), float("nan"), dtype=torch.float64, device=cuda)
+                    for q in peers}
+    dst = {q: (plans[q].recv_ranges[me][0], max(plans[q].n_ghost, 1)) for q in peers}
+    hp = DI.HaloPeer(me, peers, dst, flags_local.data_ptr(), {q: t.data_ptr() for q, t in flags_peer_t.items()},
+                     plan.n_ghost, cuda)
+    hp._opener = lambda p_, dt, nb: DI._GhostBlocks(ghost_local.data_ptr(), ghost_local,
+                                                    {q: t.data_ptr() for q, t in ghost_peer_t.items()})
+    op = DI.DistCsr(plan, None, cuda)
+    op._halo_peer = hp
+    for epoch in (1, 2, 3):
+        X = np.asfortranarray(rng.standard_normal((A.n_rows, p)))
+        ref = oracle.spmm(A.row_ptr, A.col_idx, A.values, X, nthreads=1)
+        par = epoch & 1
+        # pre-arm: the neighbours' rows of X in this rank's ghost block of that parity, and their flags
+        ghost_local[par] = torch.from_numpy(np.ascontiguousarray(X[plan.ghost_cols].T)).to(cuda)
+        for q in peers:
+            flags_local[par * 8 + q] = epoch
+        torch.cuda.synchronize()
+        Z = D.to_device_block(X[part.r0:part.r1])
+        out = D.empty_block(part.n_local, p)
+        op.apply_into(Z, out)
+        torch.cuda.synchronize()
+        hp.check()
+        assert hp.epoch == epoch
+        assert np.array_equal(D.to_numpy_block(out), ref[part.r0:part.r1])
+        for q in peers:
+            s0, s1 = plans[q].recv_ranges[me]
+            got = ghost_peer_t[q][par, :, s0:s1].cpu().numpy().T
+            want = X[plans[q].ghost_cols[s0:s1]]
+            assert np.array_equal(got, want)
+            assert int(flags_peer_t[q][par * 8 + me].item()) == epoch
+            # nothing outside this rank's segment was touched
+            rest = torch.cat([ghost_peer_t[q][par, :, :s0].flatten(), ghost_peer_t[q][par, :, s1:].flatten()])
+            assert bool(torch.isnan(rest).all().item())
+        assert int(flags_local[16].item()) == 0  # ticket re-armed
