@@ -174,7 +174,7 @@ def _exchange_recv_lists(part: RowPartition, recv_lists: dict) -> dict:
 
 def peer_eligible(infos, max_world: int = 8):
     """Can these ranks reduce through peer memory?  ``infos`` is every
-    rank's (hostname, CUDA device index or None).  Returns (ok, reason):
+    rank's (hostname, GPU UUID or device index, None without a GPU).  Returns (ok, reason):
     one node, one distinct GPU per rank, 2..max_world ranks."""
     world = len(infos)
     if world < 2:
@@ -215,7 +215,10 @@ class PeerGroup:
         if os.environ.get("RG_PEER_GRAM", "1") == "0" or not comm.nccl or not torch.cuda.is_available():
             return None
         infos = [None] * comm.world
-        dist.all_gather_object(infos, (socket.gethostname(), torch.cuda.current_device()), group=comm.group)
+        # the GPU's UUID, not its index: ranks may each see their GPU as device 0 (CUDA_VISIBLE_DEVICES)
+        props = torch.cuda.get_device_properties(torch.cuda.current_device())
+        gpu = str(getattr(props, "uuid", "")) or torch.cuda.current_device()
+        dist.all_gather_object(infos, (socket.gethostname(), gpu), group=comm.group)
         ok, why = peer_eligible(infos)
         if not ok:
             if comm.rank == 0 and comm.world > 1:
