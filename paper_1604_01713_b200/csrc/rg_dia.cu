@@ -29,6 +29,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstring>
 
 namespace rg {
@@ -217,7 +218,97 @@ static cudaError_t launch_dia(const DiaParams& P, const DiaMaps& M, cudaStream_t
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Building the layout from the CSR arrays on the device (once per matrix;
+// sparse_core.DiaPlan).  Pass 1 collects the distinct offsets col - row in a
+// 64-slot open-addressed table (after the first warps every lookup is a read
+// hit; a matrix with more offsets than slots sets the overflow word and the
+// remaining rows return at once).  Pass 2, given the sorted offsets, scatters
+// each row's values into the n x ndiag block and ORs its mask.
+// ---------------------------------------------------------------------------
+constexpr int kDiaTable = 64;
+constexpr int kDiaEmpty = INT32_MIN;
+
+__global__ void dia_offsets_kernel(int64_t n_rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                   int* table, int* overflow) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows || *reinterpret_cast<volatile int*>(overflow)) return;
+  int last = kDiaEmpty;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) {
+    const int off = ci[e] - (int)r;
+    if (off == last) continue;
+    last = off;
+    unsigned h = ((unsigned)off * 2654435761u) >> 26;  // 6 bits
+    int probes = 0;
+    for (; probes < kDiaTable; ++probes, h = (h + 1) & (kDiaTable - 1)) {
+      int cur = reinterpret_cast<volatile int*>(table)[h];
+      if (cur == off) break;
+      if (cur == kDiaEmpty) {
+        cur = atomicCAS(table + h, kDiaEmpty, off);
+        if (cur == kDiaEmpty || cur == off) break;
+      }
+    }
+    if (probes == kDiaTable) {
+      *overflow = 1;
+      return;
+    }
+  }
+}
+
+__global__ void dia_fill_kernel(int64_t n_rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double* __restrict__ v, int ndiag, const int32_t* __restrict__ offs,
+                                double* __restrict__ dia, int64_t ld, uint32_t* __restrict__ mask) {
+  __shared__ int s_off[kDiaMaxDiag];
+  if ((int)threadIdx.x < ndiag) s_off[threadIdx.x] = offs[threadIdx.x];
+  __syncthreads();
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  uint32_t m = 0;
+  int d = 0;
+  for (int e = rp[r]; e < rp[r + 1]; ++e) {
+    const int off = ci[e] - (int)r;
+    // a row's offsets ascend with its column indices: resume the scan at d
+    while (d < ndiag && s_off[d] < off) ++d;
+    dia[r + (int64_t)d * ld] = v[e];
+    m |= 1u << d;
+  }
+  mask[r] = m;
+}
+
 }  // namespace rg
+
+// distinct offsets of the matrix into d_table (64 ints, preset to INT32_MIN
+// by the caller); *d_overflow (preset 0) becomes 1 when there are more
+extern "C" int rg_dia_offsets(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, int32_t* d_table,
+                              int32_t* d_overflow, void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n_rows >= 0 && d_rp && d_table && d_overflow, "rg_dia_offsets: bad arguments");
+  if (n_rows == 0) return RG_OK;
+  dia_offsets_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, d_rp, d_ci, d_table,
+                                                                                       d_overflow);
+  RG_CHECK_LAUNCH("rg_dia_offsets");
+  count_launches(1);
+  return RG_OK;
+}
+
+// values and masks of the layout: d_dia (n_rows x ndiag, ld, zeroed by the
+// caller), d_mask (n_rows); d_offsets = the ascending offsets on the device
+extern "C" int rg_dia_fill_f64(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, const double* d_vals,
+                               int32_t ndiag, const int32_t* d_offsets, double* d_dia, int64_t ld_dia,
+                               uint32_t* d_mask, void* stream) {
+  using namespace rg;
+  clear_error();
+  RG_REQUIRE(n_rows >= 0 && ndiag >= 1 && ndiag <= kDiaMaxDiag && d_rp && d_offsets && d_dia && d_mask &&
+                 ld_dia >= n_rows,
+             "rg_dia_fill_f64: bad arguments (ndiag=%d)", ndiag);
+  if (n_rows == 0) return RG_OK;
+  dia_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      n_rows, d_rp, d_ci, d_vals, ndiag, d_offsets, d_dia, ld_dia, d_mask);
+  RG_CHECK_LAUNCH("rg_dia_fill_f64");
+  count_launches(1);
+  return RG_OK;
+}
 
 extern "C" int rg_spmm_dia_f64(int64_t n_rows, int64_t row_begin, int64_t row_end, int32_t ndiag,
                                const int32_t* h_offsets, const double* d_dia, int64_t ld_dia,

@@ -178,8 +178,22 @@ def to_device_block(x, device=None, dtype=torch.float64) -> torch.Tensor:
     return out
 
 
+PINNED_D2H_MIN, PINNED_D2H_MAX = 1 << 22, 8 << 30
+
+
 def to_numpy_block(t: torch.Tensor) -> np.ndarray:
-    """Column-major CUDA block -> Fortran-ordered numpy array (D2H)."""
+    """Column-major CUDA block -> Fortran-ordered numpy array (D2H).
+
+    Large blocks (a solution of config 4 is 1 GB) land in page-locked memory
+    from torch's caching host allocator: 20 ms at the PCIe rate instead of
+    0.47 s through a fresh pageable allocation, and the block is reused once
+    the caller drops the array."""
+    nbytes = t.numel() * t.element_size()
+    if t.is_cuda and PINNED_D2H_MIN <= nbytes <= PINNED_D2H_MAX:
+        host = torch.empty((t.shape[1], t.shape[0]), dtype=t.dtype, pin_memory=True)  # (p, n) C-order
+        host.copy_(t.t(), non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return host.numpy().T  # F-ordered view; the array keeps the pinned block alive
     host = t.t().contiguous().cpu().numpy()  # (p, n) C-order
     return np.asfortranarray(host.T)
 

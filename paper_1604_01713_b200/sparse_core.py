@@ -17,10 +17,13 @@ sparse_core.py): same names, same argument meaning, same exceptions.
 
 from __future__ import annotations
 
+import weakref
+
 import numpy as np
 import scipy.sparse as sp
 import torch
 
+from . import _lib
 from . import device as _dev
 
 
@@ -53,6 +56,10 @@ def as_device_block(x, device=None) -> torch.Tensor:
     return _dev.to_device_block(as_block(x), device)
 
 
+# (id(row_ptr), id(col_idx), device) -> (weakrefs to the host arrays, device copies)
+_STRUCT_CACHE: dict = {}
+
+
 class DeviceCsr:
     """CSR arrays resident in HBM: int32 row_ptr (n+1), int32 col_idx and
     float64 values (nnz), in the host matrix's storage order."""
@@ -83,8 +90,19 @@ class DeviceCsr:
         dev = _dev.require_cuda(device)
         if len(values) >= 2**31:
             raise ValueError("nnz >= 2^31 needs 64-bit indices (not supported)")
-        rp = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int32)).to(dev)
-        ci = torch.from_numpy(np.ascontiguousarray(col_idx, dtype=np.int32)).to(dev)
+        # matrices of a sequence share their structure arrays (A_i = A + diag):
+        # the device copies of row_ptr / col_idx are shared too
+        key = (id(row_ptr), id(col_idx), str(dev))
+        hit = _STRUCT_CACHE.get(key)
+        if hit is not None and hit[0]() is row_ptr and hit[1]() is col_idx:
+            rp, ci = hit[2], hit[3]
+        else:
+            rp = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int32)).to(dev)
+            ci = torch.from_numpy(np.ascontiguousarray(col_idx, dtype=np.int32)).to(dev)
+            if isinstance(row_ptr, np.ndarray) and isinstance(col_idx, np.ndarray):
+                if len(_STRUCT_CACHE) >= 4:
+                    _STRUCT_CACHE.pop(next(iter(_STRUCT_CACHE)))
+                _STRUCT_CACHE[key] = (weakref.ref(row_ptr), weakref.ref(col_idx), rp, ci)
         cplx = np.iscomplexobj(values)
         v = torch.from_numpy(np.ascontiguousarray(values, dtype=np.complex128 if cplx else np.float64)).to(dev)
         out = cls(n_rows, n_cols, rp, ci, v, dev)
@@ -114,20 +132,27 @@ class DiaPlan:
         if A.values.dtype != torch.float64 or A.nnz == 0 or A.n_rows == 0:
             return None
         dev = A.device
-        counts = (A.row_ptr[1:] - A.row_ptr[:-1]).long()
-        rows = torch.repeat_interleave(torch.arange(A.n_rows, device=dev), counts)
-        off = A.col_idx.long() - rows
-        uniq = torch.unique(off)
-        nd = int(uniq.numel())
-        if nd > cls.MAX_DIAG or nd * A.n_rows > cls.MAX_FILL * A.nnz:
+        L, st = _dev.lib(), _dev.stream_ptr()
+        # pass 1 (rg_dia_offsets): the distinct offsets col - row, in a 64-slot table
+        empty = np.iinfo(np.int32).min
+        table = torch.full((64,), empty, dtype=torch.int32, device=dev)
+        over = torch.zeros(1, dtype=torch.int32, device=dev)
+        _lib.check(L.rg_dia_offsets(A.n_rows, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), table.data_ptr(),
+                                    over.data_ptr(), st), "dia offsets")
+        tab = torch.cat([table, over]).cpu().numpy()
+        if tab[64]:
             return None
-        d = torch.searchsorted(uniq, off)
+        offsets = np.sort(tab[:64][tab[:64] != empty]).astype(np.int32)
+        nd = int(offsets.size)
+        if nd == 0 or nd > cls.MAX_DIAG or nd * A.n_rows > cls.MAX_FILL * A.nnz:
+            return None
+        # pass 2 (rg_dia_fill_f64): values and per-row masks
         dia = _dev.zeros_block(A.n_rows, nd, dev)
-        dia.index_put_((rows, d), A.values)
         mask = torch.zeros(_dev.round_ld(A.n_rows), dtype=torch.int32, device=dev)
-        mask.index_add_(0, rows, torch.bitwise_left_shift(torch.ones_like(d), d).to(torch.int32))
-        offsets = np.ascontiguousarray(uniq.cpu().numpy(), dtype=np.int32)
-        del counts, rows, off, d
+        offs_dev = torch.from_numpy(offsets).to(dev)
+        _lib.check(L.rg_dia_fill_f64(A.n_rows, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.values.data_ptr(), nd,
+                                     offs_dev.data_ptr(), dia.data_ptr(), _dev.ld_of(dia), mask.data_ptr(), st),
+                   "dia fill")
         return cls(offsets, dia, mask)
 
 
