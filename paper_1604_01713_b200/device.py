@@ -174,26 +174,101 @@ def to_device_block(x, device=None, dtype=torch.float64) -> torch.Tensor:
     a = np.asfortranarray(a, dtype=np_dtype)
     out = empty_block(a.shape[0], a.shape[1], dev, dtype)
     # a is F-ordered: its transpose is a C-contiguous (p, n) array
-    out.copy_(torch.from_numpy(a.T).t())
+    host = torch.from_numpy(a.T)
+    if a.nbytes >= Staging.MIN_BYTES:
+        Staging.upload([(_bytes_view(out[:, c]), _bytes_view(host[c])) for c in range(a.shape[1])])
+    else:
+        out.copy_(host.t())
     return out
 
 
-PINNED_D2H_MIN, PINNED_D2H_MAX = 1 << 22, 8 << 30
+class Staging:
+    """Large host <-> device copies through two persistent page-locked
+    chunks: the DMA of one chunk overlaps the (multi-threaded) host copy of
+    the other between the chunk and the caller's pageable array.  The
+    driver's own pageable path moves ~11 GB/s up and, into a freshly
+    allocated array, 2.3 GB/s down (page faults inside the copy); a 1 GB
+    solution came back in 0.47 s (tools/prof_setup.py)."""
+
+    CHUNK = 64 << 20
+    MIN_BYTES = 8 << 20
+    _bufs = None
+    _events = None
+
+    @classmethod
+    def _get(cls):
+        if cls._bufs is None:
+            cls._bufs = [torch.empty(cls.CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            cls._events = [torch.cuda.Event() for _ in range(2)]
+        return cls._bufs, cls._events
+
+    @classmethod
+    def _segments(cls, dev_flat: torch.Tensor, host_flat: torch.Tensor):
+        n = dev_flat.numel()
+        return [(dev_flat[o: o + cls.CHUNK], host_flat[o: o + cls.CHUNK]) for o in range(0, n, cls.CHUNK)]
+
+    @classmethod
+    def download(cls, pairs) -> None:
+        """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)], same lengths."""
+        bufs, evs = cls._get()
+        segs = [sg for d, h in pairs for sg in cls._segments(d, h)]
+        stream = torch.cuda.current_stream()
+        prev = None
+        for j, (d, h) in enumerate(segs):
+            b = j & 1
+            bufs[b][: d.numel()].copy_(d, non_blocking=True)
+            evs[b].record(stream)
+            if prev is not None:
+                pb, ph = prev
+                evs[pb].synchronize()
+                ph.copy_(bufs[pb][: ph.numel()])
+            prev = (b, h)
+        if prev is not None:
+            pb, ph = prev
+            evs[pb].synchronize()
+            ph.copy_(bufs[pb][: ph.numel()])
+
+    @classmethod
+    def upload(cls, pairs) -> None:
+        """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)]; returns once
+        every chunk is enqueued (the host array may be reused: it has been read)."""
+        bufs, evs = cls._get()
+        segs = [sg for d, h in pairs for sg in cls._segments(d, h)]
+        stream = torch.cuda.current_stream()
+        for j, (d, h) in enumerate(segs):
+            b = j & 1
+            if j >= 2:
+                evs[b].synchronize()  # the DMA that last read this chunk has finished
+            bufs[b][: h.numel()].copy_(h)
+            d.copy_(bufs[b][: h.numel()], non_blocking=True)
+            evs[b].record(stream)
+        for e in evs[: min(2, len(segs))]:
+            e.synchronize()  # the chunks are free for the next call
+
+
+def _bytes_view(t: torch.Tensor) -> torch.Tensor:
+    return t.reshape(-1).view(torch.uint8)
+
+
+def upload_array(a: np.ndarray, device) -> torch.Tensor:
+    """1-D contiguous host array -> CUDA tensor (staged when large)."""
+    h = torch.from_numpy(a)
+    if h.numel() * h.element_size() < Staging.MIN_BYTES:
+        return h.to(device)
+    out = torch.empty(h.shape, dtype=h.dtype, device=device)
+    Staging.upload([(_bytes_view(out), _bytes_view(h))])
+    return out
 
 
 def to_numpy_block(t: torch.Tensor) -> np.ndarray:
-    """Column-major CUDA block -> Fortran-ordered numpy array (D2H).
-
-    Large blocks (a solution of config 4 is 1 GB) land in page-locked memory
-    from torch's caching host allocator: 20 ms at the PCIe rate instead of
-    0.47 s through a fresh pageable allocation, and the block is reused once
-    the caller drops the array."""
+    """Column-major CUDA block -> Fortran-ordered numpy array (D2H; large
+    blocks through the page-locked staging chunks)."""
     nbytes = t.numel() * t.element_size()
-    if t.is_cuda and PINNED_D2H_MIN <= nbytes <= PINNED_D2H_MAX:
-        host = torch.empty((t.shape[1], t.shape[0]), dtype=t.dtype, pin_memory=True)  # (p, n) C-order
-        host.copy_(t.t(), non_blocking=True)
-        torch.cuda.current_stream(t.device).synchronize()
-        return host.numpy().T  # F-ordered view; the array keeps the pinned block alive
+    if t.is_cuda and t.dim() == 2 and nbytes >= Staging.MIN_BYTES and is_col_major(t):
+        n, p = t.shape
+        host = torch.empty((p, n), dtype=t.dtype)  # (p, n) C-order == (n, p) F-order
+        Staging.download([(_bytes_view(t[:, c]), _bytes_view(host[c])) for c in range(p)])
+        return host.numpy().T
     host = t.t().contiguous().cpu().numpy()  # (p, n) C-order
     return np.asfortranarray(host.T)
 

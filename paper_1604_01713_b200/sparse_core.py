@@ -97,14 +97,14 @@ class DeviceCsr:
         if hit is not None and hit[0]() is row_ptr and hit[1]() is col_idx:
             rp, ci = hit[2], hit[3]
         else:
-            rp = torch.from_numpy(np.ascontiguousarray(row_ptr, dtype=np.int32)).to(dev)
-            ci = torch.from_numpy(np.ascontiguousarray(col_idx, dtype=np.int32)).to(dev)
+            rp = _dev.upload_array(np.ascontiguousarray(row_ptr, dtype=np.int32), dev)
+            ci = _dev.upload_array(np.ascontiguousarray(col_idx, dtype=np.int32), dev)
             if isinstance(row_ptr, np.ndarray) and isinstance(col_idx, np.ndarray):
                 if len(_STRUCT_CACHE) >= 4:
                     _STRUCT_CACHE.pop(next(iter(_STRUCT_CACHE)))
                 _STRUCT_CACHE[key] = (weakref.ref(row_ptr), weakref.ref(col_idx), rp, ci)
         cplx = np.iscomplexobj(values)
-        v = torch.from_numpy(np.ascontiguousarray(values, dtype=np.complex128 if cplx else np.float64)).to(dev)
+        v = _dev.upload_array(np.ascontiguousarray(values, dtype=np.complex128 if cplx else np.float64), dev)
         out = cls(n_rows, n_cols, rp, ci, v, dev)
         out.host_row_ptr = np.asarray(row_ptr)
         return out
