@@ -178,10 +178,12 @@ def test_tall_narrow_ring_passes(cuda, n, p):
     G = D.small(p, p)
     D.tall(poisoned(Z), None, r1=r1, gram=("self", G))
     assert _rel(G.cpu().numpy(), q1.T @ q1) <= 1e-12
-    # K_g: two solves, stored in place
+    # K_g: two solves, stored in place; nothing outside the n x p block is written
     Zd = poisoned(Z)
     D.tall(Zd, Zd, r1=r1, r2=r2)
     assert _rel(D.to_numpy_block(Zd), q2) <= 1e-12
+    whole = torch.as_strided(Zd, (D.round_ld(n), p + 3), (1, D.round_ld(n)))
+    assert bool(torch.isnan(whole[n:, :]).all()) and bool(torch.isnan(whole[:, p:]).all())
     # solve + store + norms of the result
     Zo = poisoned(np.zeros((n, p)))
     ss = torch.zeros(p, dtype=torch.float64, device=cuda)
