@@ -13,6 +13,7 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import os
+import threading
 
 import numpy as np
 import torch
@@ -194,6 +195,7 @@ class Staging:
     MIN_BYTES = 8 << 20
     _bufs = None
     _events = None
+    _lock = threading.Lock()  # one transfer at a time owns the two chunks
 
     @classmethod
     def _get(cls):
@@ -210,6 +212,11 @@ class Staging:
     @classmethod
     def download(cls, pairs) -> None:
         """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)], same lengths."""
+        with cls._lock:
+            cls._download(pairs)
+
+    @classmethod
+    def _download(cls, pairs) -> None:
         bufs, evs = cls._get()
         segs = [sg for d, h in pairs for sg in cls._segments(d, h)]
         stream = torch.cuda.current_stream()
@@ -232,6 +239,11 @@ class Staging:
     def upload(cls, pairs) -> None:
         """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)]; returns once
         every chunk is enqueued (the host array may be reused: it has been read)."""
+        with cls._lock:
+            cls._upload(pairs)
+
+    @classmethod
+    def _upload(cls, pairs) -> None:
         bufs, evs = cls._get()
         segs = [sg for d, h in pairs for sg in cls._segments(d, h)]
         stream = torch.cuda.current_stream()
