@@ -486,8 +486,11 @@ def _enqueue_cgs2(fact, opA, recycle, m, hb, ahat, graphs=False) -> _PendingStep
              and (joint or (k_ <= _dev.MAX_GC and w_ <= _dev.MAX_GC)))
     owner = _capturable(opA)
     enq = None
+    # (a row-partitioned step is never replayed: a captured Gram pass would carry
+    # the epoch of its capture into every replay of the in-kernel reduction)
     if (graphs and fused and owner is not None and fact._ws is not None and fact._ws.graphs is not None
-            and fact.n <= GRAPH_MAX_ROWS and not _dev.LaunchLog.timing and hb is fact._hb and ahat is fact._ahat):
+            and fact.n <= GRAPH_MAX_ROWS and not _dev.LaunchLog.timing and hb is fact._hb and ahat is fact._ahat
+            and _dev.get_comm() is None):
         enq = _replay_step(fact, opA, owner, C, m, joint)
     if enq is None:
         saved = fact._ahat
