@@ -124,7 +124,8 @@ __device__ __forceinline__ void peer_allreduce(const PeerComm& C, double* g, int
     peer_st_release(C.flags[tid] + par * kPeerMaxWorld + C.rank, C.epoch);
     const unsigned* f = C.flags[C.rank] + par * kPeerMaxWorld + tid;
     const long long t0 = clock64();
-    while (peer_ld_acquire(f) != C.epoch) {
+    // (epochs only grow: a flag at or past this epoch means the peer's values are in place)
+    while ((int)(peer_ld_acquire(f) - C.epoch) < 0) {
       if (clock64() - t0 > C.timeout) {  // a peer never arrived: flag it, do not hang the device
         C.flags[C.rank][2 * kPeerMaxWorld] = C.epoch;
         break;

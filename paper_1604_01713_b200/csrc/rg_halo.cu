@@ -62,7 +62,7 @@ __global__ void halo_wait_kernel(const unsigned* flags, HaloWait W, unsigned epo
   if ((int)threadIdx.x < W.n) {
     const unsigned* f = flags + W.peer[threadIdx.x];
     const long long t0 = clock64();
-    while (peer_ld_acquire(f) != epoch) {
+    while ((int)(peer_ld_acquire(f) - epoch) < 0) {
       if (clock64() - t0 > timeout) {
         *err = epoch;
         break;

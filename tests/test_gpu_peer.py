@@ -282,3 +282,44 @@ def test_halo_push_with_prearmed_neighbours(cuda, me, p):
             rest = torch.cat([ghost_peer_t[q][par, :, :s0].flatten(), ghost_peer_t[q][par, :, s1:].flatten()])
             assert bool(torch.isnan(rest).all().item())
         assert int(flags_local[16].item()) == 0  # ticket re-armed
+
+
+def test_solver_with_a_silent_peer_is_bitwise_the_single_process_solve(cuda):
+    """End to end on one GPU: a peer group of 2 whose other rank has
+    'already arrived' at every epoch (its flags pre-set far ahead) and
+    contributes zeros.  Every Gram / norm pass of a full GCRO-DR sequence --
+    through the fused orchestrators rg_cgs2_f64 / rg_cholqr2_f64 -- then runs
+    the in-kernel reduction, and adding the peer's zeros must leave cycles,
+    matvec counts, residual histories and solutions bit for bit those of the
+    plain run."""
+    from paper_1604_01713_b200 import SolverConfig, _lib, device as D, problems, solve_sequence
+
+    L = D.lib()
+    systems, kw = problems.cfg1_sequence()
+    plain = solve_sequence(systems, SolverConfig(**kw))
+    nb = L.rg_peer_buffer_bytes()
+    bufs = [torch.zeros(nb, dtype=torch.uint8, device=cuda) for _ in range(2)]
+    slot_bytes = 2 * 8 * 4096 * 8
+    flags = bufs[0][slot_bytes:].view(torch.int32)
+    flags[0 * 8 + 1] = 0x7FFFFFFF  # rank 1, both parities: ahead of every epoch
+    flags[1 * 8 + 1] = 0x7FFFFFFF
+    torch.cuda.synchronize()
+    arr = (ctypes.c_void_p * 2)(bufs[0].data_ptr(), bufs[1].data_ptr())
+    _lib.check(L.rg_peer_set(2, 0, arr, 2.0), "peer set")
+    try:
+        before = L.rg_launch_count()
+        peer = solve_sequence(systems, SolverConfig(**kw))
+        assert L.rg_launch_count() > before
+        e = ctypes.c_uint32(0)
+        _lib.check(L.rg_peer_error(ctypes.byref(e), D.stream_ptr()), "peer error")
+        assert e.value == 0
+    finally:
+        L.rg_peer_clear()
+    # rank 0 really exchanged: its last Grams and epochs sit in the stand-in for rank 1's buffer
+    sent_flags = bufs[1][slot_bytes:].view(torch.int32)
+    assert int(sent_flags[0].item()) > 1000 and int(sent_flags[8].item()) > 1000
+    for a, b in zip(plain, peer):
+        assert a.error is None and b.error is None
+        assert a.cycles == b.cycles and a.matvec_count == b.matvec_count
+        assert np.array_equal(np.concatenate(a.residual_history), np.concatenate(b.residual_history))
+        assert np.array_equal(a.solution, b.solution)
