@@ -786,20 +786,19 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        # the CPU arm: rank 0 alone runs and prints it, the other ranks exit 0 without
+        # work (no process group: nothing is exchanged)
+        run_reference(args, rank, world)
+        return
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        if args.impl == "reference":
-            dist.init_process_group("gloo")
-        else:
-            import torch
-
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1))
-            # RG_BENCH_BACKEND=gloo runs the N>1 code path on a single GPU (test only)
-            dist.init_process_group(os.environ.get("RG_BENCH_BACKEND", "nccl"))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-    elif args.workload == "solve":
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1))
+        # RG_BENCH_BACKEND=gloo runs the N>1 code path on a single GPU (test only)
+        dist.init_process_group(os.environ.get("RG_BENCH_BACKEND", "nccl"))
+    if args.workload == "solve":
         run_solve(args, rank, world)
     elif args.workload == "ortho":
         run_ortho(args, rank, world)
