@@ -86,15 +86,20 @@ int rg_spmm_dia_f64(int64_t n_rows, int64_t row_begin, int64_t row_end, int32_t 
 /*
  * The diagonal layout built from the CSR arrays on the device, once per
  * matrix (no reference counterpart: the reference keeps CSR only).
- *   rg_dia_offsets   distinct offsets col - row into d_table (64 int32, preset
- *                    to INT32_MIN); *d_overflow (preset 0) = 1 if more exist
+ *   rg_dia_offsets   distinct offsets col - row of rows [row_begin, row_end)
+ *                    into d_table (64 int32, preset to INT32_MIN);
+ *                    *d_overflow (preset 0) = 1 if more exist
  *   rg_dia_fill_f64  values into d_dia (n_rows x ndiag, zeroed) and per-row
- *                    masks, given the ascending offsets on the device
+ *                    masks (zeroed) for those rows, given the ascending
+ *                    offsets on the device.  A layout built over a sub-range
+ *                    (the interior rows of a row partition, which reference
+ *                    owned columns only) serves products inside that range.
  */
-int rg_dia_offsets(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, int32_t* d_table, int32_t* d_overflow,
-                   void* stream);
-int rg_dia_fill_f64(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, const double* d_vals, int32_t ndiag,
-                    const int32_t* d_offsets, double* d_dia, int64_t ld_dia, uint32_t* d_mask, void* stream);
+int rg_dia_offsets(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_rp, const int32_t* d_ci,
+                   int32_t* d_table, int32_t* d_overflow, void* stream);
+int rg_dia_fill_f64(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_rp, const int32_t* d_ci,
+                    const double* d_vals, int32_t ndiag, const int32_t* d_offsets, double* d_dia, int64_t ld_dia,
+                    uint32_t* d_mask, void* stream);
 
 /*
  * Fused tall-skinny "update, triangular solve, Gram" pass over an n x p

@@ -58,8 +58,9 @@ PROTOTYPES = {
     "rg_gather_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr]),
     "rg_spmm_dia_f64": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_i64,
                                        c_i32, c_ptr, c_i64, c_ptr, c_ptr]),
-    "rg_dia_offsets": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
-    "rg_dia_fill_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
+    "rg_dia_offsets": (ctypes.c_int, [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr]),
+    "rg_dia_fill_f64": (ctypes.c_int, [c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_i64, c_ptr,
+                                       c_ptr]),
     "rg_halo_pack": (ctypes.c_int, [c_i64, c_i32, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "rg_permute_rows_f64": (ctypes.c_int, [c_i64, c_i32, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_ptr]),
     "rg_sptrsv_perm_f64": (ctypes.c_int, [c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_i32, c_ptr,

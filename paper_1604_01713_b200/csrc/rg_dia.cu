@@ -229,10 +229,10 @@ static cudaError_t launch_dia(const DiaParams& P, const DiaMaps& M, cudaStream_t
 constexpr int kDiaTable = 64;
 constexpr int kDiaEmpty = INT32_MIN;
 
-__global__ void dia_offsets_kernel(int64_t n_rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                   int* table, int* overflow) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_rows || *reinterpret_cast<volatile int*>(overflow)) return;
+__global__ void dia_offsets_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
+                                   const int32_t* __restrict__ ci, int* table, int* overflow) {
+  const int64_t r = row_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= row_end || *reinterpret_cast<volatile int*>(overflow)) return;
   int last = kDiaEmpty;
   for (int e = rp[r]; e < rp[r + 1]; ++e) {
     const int off = ci[e] - (int)r;
@@ -255,14 +255,15 @@ __global__ void dia_offsets_kernel(int64_t n_rows, const int32_t* __restrict__ r
   }
 }
 
-__global__ void dia_fill_kernel(int64_t n_rows, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                const double* __restrict__ v, int ndiag, const int32_t* __restrict__ offs,
-                                double* __restrict__ dia, int64_t ld, uint32_t* __restrict__ mask) {
+__global__ void dia_fill_kernel(int64_t row_begin, int64_t row_end, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, const double* __restrict__ v, int ndiag,
+                                const int32_t* __restrict__ offs, double* __restrict__ dia, int64_t ld,
+                                uint32_t* __restrict__ mask) {
   __shared__ int s_off[kDiaMaxDiag];
   if ((int)threadIdx.x < ndiag) s_off[threadIdx.x] = offs[threadIdx.x];
   __syncthreads();
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
+  const int64_t r = row_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= row_end) return;
   uint32_t m = 0;
   int d = 0;
   for (int e = rp[r]; e < rp[r + 1]; ++e) {
@@ -277,34 +278,40 @@ __global__ void dia_fill_kernel(int64_t n_rows, const int32_t* __restrict__ rp, 
 
 }  // namespace rg
 
-// distinct offsets of the matrix into d_table (64 ints, preset to INT32_MIN
-// by the caller); *d_overflow (preset 0) becomes 1 when there are more
-extern "C" int rg_dia_offsets(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, int32_t* d_table,
-                              int32_t* d_overflow, void* stream) {
+// distinct offsets of rows [row_begin, row_end) into d_table (64 ints, preset
+// to INT32_MIN by the caller); *d_overflow (preset 0) becomes 1 when there
+// are more
+extern "C" int rg_dia_offsets(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_rp,
+                              const int32_t* d_ci, int32_t* d_table, int32_t* d_overflow, void* stream) {
   using namespace rg;
   clear_error();
-  RG_REQUIRE(n_rows >= 0 && d_rp && d_table && d_overflow, "rg_dia_offsets: bad arguments");
-  if (n_rows == 0) return RG_OK;
-  dia_offsets_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(n_rows, d_rp, d_ci, d_table,
-                                                                                       d_overflow);
+  RG_REQUIRE(n_rows >= 0 && 0 <= row_begin && row_begin <= row_end && row_end <= n_rows && d_rp && d_table &&
+                 d_overflow,
+             "rg_dia_offsets: bad arguments");
+  if (row_end == row_begin) return RG_OK;
+  dia_offsets_kernel<<<(unsigned)((row_end - row_begin + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      row_begin, row_end, d_rp, d_ci, d_table, d_overflow);
   RG_CHECK_LAUNCH("rg_dia_offsets");
   count_launches(1);
   return RG_OK;
 }
 
-// values and masks of the layout: d_dia (n_rows x ndiag, ld, zeroed by the
-// caller), d_mask (n_rows); d_offsets = the ascending offsets on the device
-extern "C" int rg_dia_fill_f64(int64_t n_rows, const int32_t* d_rp, const int32_t* d_ci, const double* d_vals,
-                               int32_t ndiag, const int32_t* d_offsets, double* d_dia, int64_t ld_dia,
-                               uint32_t* d_mask, void* stream) {
+// values and masks of rows [row_begin, row_end) of the layout: d_dia (n_rows
+// x ndiag, ld, zeroed by the caller), d_mask (n_rows, zeroed); d_offsets = the
+// ascending offsets on the device.  Rows outside the range keep mask 0: the
+// layout then serves products over sub-ranges of [row_begin, row_end) only
+// (the interior rows of a row partition, whose entries are all owned columns)
+extern "C" int rg_dia_fill_f64(int64_t n_rows, int64_t row_begin, int64_t row_end, const int32_t* d_rp,
+                               const int32_t* d_ci, const double* d_vals, int32_t ndiag, const int32_t* d_offsets,
+                               double* d_dia, int64_t ld_dia, uint32_t* d_mask, void* stream) {
   using namespace rg;
   clear_error();
-  RG_REQUIRE(n_rows >= 0 && ndiag >= 1 && ndiag <= kDiaMaxDiag && d_rp && d_offsets && d_dia && d_mask &&
-                 ld_dia >= n_rows,
+  RG_REQUIRE(n_rows >= 0 && 0 <= row_begin && row_begin <= row_end && row_end <= n_rows && ndiag >= 1 &&
+                 ndiag <= kDiaMaxDiag && d_rp && d_offsets && d_dia && d_mask && ld_dia >= n_rows,
              "rg_dia_fill_f64: bad arguments (ndiag=%d)", ndiag);
-  if (n_rows == 0) return RG_OK;
-  dia_fill_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      n_rows, d_rp, d_ci, d_vals, ndiag, d_offsets, d_dia, ld_dia, d_mask);
+  if (row_end == row_begin) return RG_OK;
+  dia_fill_kernel<<<(unsigned)((row_end - row_begin + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      row_begin, row_end, d_rp, d_ci, d_vals, ndiag, d_offsets, d_dia, ld_dia, d_mask);
   RG_CHECK_LAUNCH("rg_dia_fill_f64");
   count_launches(1);
   return RG_OK;

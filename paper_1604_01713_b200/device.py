@@ -426,7 +426,8 @@ def spmm(dcsr, X: torch.Tensor, Y: torch.Tensor, row_begin: int = 0, row_end: in
     if cplx != (dcsr.values.dtype == torch.complex128) or Y.dtype != X.dtype:
         raise TypeError(f"spmm: matrix values {dcsr.values.dtype}, block {X.dtype}, output {Y.dtype} must agree")
     plan = dcsr.dia() if (not cplx and Xg is None and SPMM_DIA and hasattr(dcsr, "dia")) else None
-    if plan is not None and X.numel() and is_col_major(X) and ld_of(X) % 2 == 0 and X.data_ptr() % 16 == 0:
+    if (plan is not None and plan.covers(row_begin, row_end) and X.numel() and is_col_major(X)
+            and ld_of(X) % 2 == 0 and X.data_ptr() % 16 == 0):
         # stencil-like matrix: the diagonal-layout kernel (same arithmetic, bitwise)
         offs = plan.offsets
         rc = L.rg_spmm_dia_f64(n_rows, row_begin, row_end, len(offs), offs.ctypes.data, plan.dia.data_ptr(),

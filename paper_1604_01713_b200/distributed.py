@@ -556,6 +556,9 @@ class DistCsr:
 
             self.dcsr = DeviceCsr.from_host(self.n_rows, self.n_rows + plan.n_ghost, plan.row_ptr, plan.col_idx,
                                             plan.values, device)
+            # the diagonal-layout SpMM serves the interior rows (owned columns only:
+            # the stencil's own diagonals); boundary rows read ghosts through the CSR kernel
+            self.dcsr.dia_rows = plan.interior
             dev = self.dcsr.device
         else:
             self.dcsr = None

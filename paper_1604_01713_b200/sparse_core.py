@@ -64,7 +64,8 @@ class DeviceCsr:
     """CSR arrays resident in HBM: int32 row_ptr (n+1), int32 col_idx and
     float64 values (nnz), in the host matrix's storage order."""
 
-    __slots__ = ("n_rows", "n_cols", "nnz", "row_ptr", "col_idx", "values", "device", "host_row_ptr", "_dia")
+    __slots__ = ("n_rows", "n_cols", "nnz", "row_ptr", "col_idx", "values", "device", "host_row_ptr", "_dia",
+                 "dia_rows")
 
     def __init__(self, n_rows, n_cols, row_ptr, col_idx, values, device):
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
@@ -75,13 +76,17 @@ class DeviceCsr:
         self.nnz = int(values.shape[0])
         self.host_row_ptr = None
         self._dia = False  # not yet analysed; None: not a diagonal matrix
+        # rows the diagonal layout covers (None: all).  A row-partitioned operator
+        # sets its interior range: only those rows reference owned columns alone
+        self.dia_rows = None
 
     def dia(self):
         """The diagonal layout of this matrix (``DiaPlan``), built on the
         device on first use, or None when its nonzeros do not lie on a few
         well-filled diagonals (the CSR kernel then runs)."""
         if self._dia is False:
-            self._dia = DiaPlan.build(self)
+            r0, r1 = self.dia_rows if self.dia_rows is not None else (0, self.n_rows)
+            self._dia = DiaPlan.build(self, int(r0), int(r1))
         return self._dia
 
 
@@ -122,14 +127,18 @@ class DiaPlan:
     MAX_DIAG = 32
     MAX_FILL = 1.25  # ndiag * n_rows <= MAX_FILL * nnz
 
-    __slots__ = ("offsets", "dia", "mask")
+    __slots__ = ("offsets", "dia", "mask", "rows")
 
-    def __init__(self, offsets, dia, mask):
-        self.offsets, self.dia, self.mask = offsets, dia, mask
+    def __init__(self, offsets, dia, mask, rows):
+        self.offsets, self.dia, self.mask, self.rows = offsets, dia, mask, rows
+
+    def covers(self, row_begin: int, row_end: int) -> bool:
+        return self.rows[0] <= row_begin and row_end <= self.rows[1]
 
     @classmethod
-    def build(cls, A: "DeviceCsr"):
-        if A.values.dtype != torch.float64 or A.nnz == 0 or A.n_rows == 0:
+    def build(cls, A: "DeviceCsr", r0: int = 0, r1: int | None = None):
+        r1 = A.n_rows if r1 is None else r1
+        if A.values.dtype != torch.float64 or A.nnz == 0 or r1 <= r0:
             return None
         dev = A.device
         L, st = _dev.lib(), _dev.stream_ptr()
@@ -137,7 +146,7 @@ class DiaPlan:
         empty = np.iinfo(np.int32).min
         table = torch.full((64,), empty, dtype=torch.int32, device=dev)
         over = torch.zeros(1, dtype=torch.int32, device=dev)
-        _lib.check(L.rg_dia_offsets(A.n_rows, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), table.data_ptr(),
+        _lib.check(L.rg_dia_offsets(A.n_rows, r0, r1, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), table.data_ptr(),
                                     over.data_ptr(), st), "dia offsets")
         tab = torch.cat([table, over]).cpu().numpy()
         if tab[64]:
@@ -150,10 +159,10 @@ class DiaPlan:
         dia = _dev.zeros_block(A.n_rows, nd, dev)
         mask = torch.zeros(_dev.round_ld(A.n_rows), dtype=torch.int32, device=dev)
         offs_dev = torch.from_numpy(offsets).to(dev)
-        _lib.check(L.rg_dia_fill_f64(A.n_rows, A.row_ptr.data_ptr(), A.col_idx.data_ptr(), A.values.data_ptr(), nd,
-                                     offs_dev.data_ptr(), dia.data_ptr(), _dev.ld_of(dia), mask.data_ptr(), st),
-                   "dia fill")
-        return cls(offsets, dia, mask)
+        _lib.check(L.rg_dia_fill_f64(A.n_rows, r0, r1, A.row_ptr.data_ptr(), A.col_idx.data_ptr(),
+                                     A.values.data_ptr(), nd, offs_dev.data_ptr(), dia.data_ptr(), _dev.ld_of(dia),
+                                     mask.data_ptr(), st), "dia fill")
+        return cls(offsets, dia, mask, (r0, r1))
 
 
 def _validate(n_rows, n_cols, rp, ci, v):

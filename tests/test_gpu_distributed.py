@@ -126,3 +126,36 @@ def _cfg5_worker(rank, world):
 
 def test_complex_sequence_two_ranks_one_gpu(cuda):
     _run(2, _cfg5_worker)
+
+
+def _dist_spmm_3d_worker(rank, world):
+    """3-D stencil, plane-aligned partition: the interior rows run on the
+    diagonal layout built over the interior range only (the renumbered ghost
+    columns would otherwise add far diagonals), the boundary rows on the CSR
+    kernel; the product is bitwise the single-process one."""
+    import torch
+
+    import oracle
+    from paper_1604_01713_b200 import device as D, distributed, problems
+
+    torch.cuda.set_device(0)
+    grid = 24
+    A = problems.conv_diff_3d(grid, 20.0)
+    X = np.asfortranarray(np.random.default_rng(3).standard_normal((A.n_rows, 8)))
+    ref = oracle.spmm(A.row_ptr, A.col_idx, A.values, X, nthreads=1)
+    op, part = distributed.setup(A, align=grid * grid)
+    try:
+        plan = op.dcsr.dia()
+        assert plan is not None and plan.rows == tuple(op.plan.interior) and len(plan.offsets) == 7
+        for p in (8, 3):
+            Z = D.to_device_block(X[part.r0:part.r1, :p])
+            out = D.empty_block(part.n_local, p)
+            op.apply_into(Z, out)
+            assert np.array_equal(D.to_numpy_block(out), ref[part.r0:part.r1, :p])
+    finally:
+        distributed.teardown()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_spmm_3d_stencil_ranks_on_one_gpu(cuda, world):
+    _run(world, _dist_spmm_3d_worker)
