@@ -204,15 +204,22 @@ class PeerGroup:
     def __init__(self, comm, local, mapped, timeout_s):
         self.comm, self.local, self.mapped, self.timeout_s = comm, local, mapped, timeout_s
         self.halos = []  # HaloPeer objects of the operators built on this group
+        self.ptrs = []
 
     @classmethod
-    def create(cls, comm: "CommContext", timeout_s: float = 20.0):
+    def create(cls, comm: "CommContext", timeout_s: float = 20.0, *, force: bool = False, selftest: bool = True):
+        """``force`` / ``selftest=False`` (tests): map the buffers whatever the
+        backend and GPU placement, and skip the known-answer reduction -- two
+        processes sharing one GPU can check the IPC plumbing with host
+        barriers, but must not launch kernels that wait on each other."""
         import ctypes
         import os
         import socket
         import sys
 
-        if os.environ.get("RG_PEER_GRAM", "1") == "0" or not comm.nccl or not torch.cuda.is_available():
+        if not torch.cuda.is_available():
+            return None
+        if not force and (os.environ.get("RG_PEER_GRAM", "1") == "0" or not comm.nccl):
             return None
         infos = [None] * comm.world
         # the GPU's UUID, not its index: ranks may each see their GPU as device 0 (CUDA_VISIBLE_DEVICES)
@@ -220,7 +227,7 @@ class PeerGroup:
         gpu = str(getattr(props, "uuid", "")) or torch.cuda.current_device()
         dist.all_gather_object(infos, (socket.gethostname(), gpu), group=comm.group)
         ok, why = peer_eligible(infos)
-        if not ok:
+        if not ok and not force:
             if comm.rank == 0 and comm.world > 1:
                 print(f"[rgb200] peer-memory Gram reduction off: {why}", file=sys.stderr)
             return None
@@ -241,9 +248,10 @@ class PeerGroup:
             ptrs.append(q.value)
             mapped.append(q.value)
         # all ranks agree on the outcome before anything is registered
-        flag = torch.tensor([1 if failed else 0], device="cuda")
+        flag = torch.tensor([1 if failed else 0], device="cuda" if comm.nccl else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=comm.group)
         self = cls(comm, buf.value, mapped, timeout_s)
+        self.ptrs = list(ptrs)  # rank r's buffer as mapped here (ptrs[rank] = the local one)
         if int(flag.item()):
             self._release()
             if comm.rank == 0:
@@ -251,6 +259,9 @@ class PeerGroup:
             return None
         arr = (ctypes.c_void_p * comm.world)(*ptrs)
         dist.barrier(group=comm.group)
+        if not selftest:
+            _lib.check(L.rg_peer_set(comm.world, comm.rank, arr, timeout_s), "peer set")
+            return self
         _lib.check(L.rg_peer_set(comm.world, comm.rank, arr, cls.SELFTEST_TIMEOUT_S), "peer set")
         # self-test: one reduction of known values, bounded wait
         t = torch.full((8,), float(comm.rank + 1), dtype=torch.float64, device="cuda")

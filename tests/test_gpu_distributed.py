@@ -159,3 +159,65 @@ def _dist_spmm_3d_worker(rank, world):
 @pytest.mark.parametrize("world", [2, 3])
 def test_distributed_spmm_3d_stencil_ranks_on_one_gpu(cuda, world):
     _run(world, _dist_spmm_3d_worker)
+
+
+def _peer_plumbing_worker(rank, world):
+    """The real multi-process plumbing of the peer-memory paths, with the two
+    ranks sharing one GPU: buffers allocated, IPC handles exchanged, peers'
+    buffers mapped, the group registered; the halo pushes of a 3-D stencil
+    land in the neighbour's ghost block with the epoch flag.  Host barriers
+    separate writers from readers -- no kernel here waits on another rank's
+    (the waits themselves are covered by the one-process emulations in
+    test_gpu_peer.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_01713_b200 import device as D, distributed as DI, problems
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L = D.lib()
+    comm = DI.CommContext(peer=False)
+    pg = DI.PeerGroup.create(comm, force=True, selftest=False)
+    assert pg is not None and L.rg_peer_active() == world and len(pg.ptrs) == world
+    comm.peer = pg
+    try:
+        # every rank's exchange buffer is visible through every other rank's mapping
+        mine = DI._wrap(pg.ptrs[rank], (4,), torch.float64, dev)
+        mine.fill_(float(rank + 1))
+        torch.cuda.synchronize()
+        dist.barrier()
+        for r in range(world):
+            assert float(DI._wrap(pg.ptrs[r], (4,), torch.float64, dev)[0].item()) == r + 1
+        dist.barrier()
+        mine.zero_()
+        torch.cuda.synchronize()
+        # halo pushes of a plane-partitioned 3-D operator
+        grid, p = 12, 5
+        A = problems.conv_diff_3d(grid, 20.0)
+        X = np.asfortranarray(np.random.default_rng(4).standard_normal((A.n_rows, p)))
+        part = DI.RowPartition.even(A.n_rows, world, rank, align=grid * grid)
+        rp, ci, v = DI.csr_row_block(A.row_ptr, A.col_idx, A.values, part.r0, part.r1)
+        plan = DI.HaloPlan.from_local_rows(part, rp, ci, v)
+        op = DI.DistCsr(plan, comm, dev)
+        hp = op._halo_peer
+        assert hp is not None and hp in pg.halos and hp.peers == [q for q in range(world) if abs(q - rank) == 1]
+        Z = D.to_device_block(X[part.r0:part.r1])
+        gb = hp.ghost(p, torch.float64)  # collective: ghost blocks allocated, exchanged, mapped
+        for epoch in (1, 2):
+            par = hp.push_all(Z, op._send_idx, gb)
+            torch.cuda.synchronize()
+            dist.barrier()
+            assert par == epoch & 1
+            got = gb.local[par].t()[: plan.n_ghost].cpu().numpy()
+            assert np.array_equal(got, X[plan.ghost_cols])  # the neighbours' rows, in ghost order
+            flags = DI._wrap(hp.flags_local, (hp.FLAG_WORDS,), torch.int32, dev).cpu().numpy()
+            assert all(flags[par * 8 + q] == epoch for q in hp.peers) and flags[16] == 0 and flags[17] == 0
+            dist.barrier()
+    finally:
+        comm.close()
+    assert L.rg_peer_active() == 0
+
+
+def test_peer_memory_plumbing_two_processes_one_gpu(cuda):
+    _run(2, _peer_plumbing_worker)
