@@ -220,13 +220,24 @@ class CpuStepSample:
 
 def cpu_step_rate(steps, warmup, sample=None):
     s = sample or CpuStepSample()
-    for i in range(warmup):
-        s.run(i)
+    # the dense part uses every host thread the SpMM does, whatever OMP_NUM_THREADS
+    # says (torchrun exports OMP_NUM_THREADS=1 to its ranks)
+    try:
+        from threadpoolctl import threadpool_limits
+
+        blas = threadpool_limits(limits=s.threads, user_api="blas")
+    except Exception:  # pragma: no cover - threadpoolctl is in the image
+        import contextlib
+
+        blas = contextlib.nullcontext()
     ts, bs = [], []
-    for i in range(steps):
-        t, b = s.run(warmup + i)
-        ts.append(t)
-        bs.append(b)
+    with blas:
+        for i in range(warmup):
+            s.run(i)
+        for i in range(steps):
+            t, b = s.run(warmup + i)
+            ts.append(t)
+            bs.append(b)
     rate = sum(bs) / sum(ts) / 1e9
     info = {"kind": "port", "cores": s.threads, "sample": s.describe(steps, warmup),
             "window_s_mean": statistics.mean(ts),
