@@ -196,6 +196,21 @@ class Staging:
     _bufs = None
     _events = None
     _lock = threading.Lock()  # one transfer at a time owns the two chunks
+    # host-copy threads for the duration of a transfer (launchers such as torchrun
+    # export OMP_NUM_THREADS=1, which would leave the chunk copies single-threaded)
+    THREADS = max(1, min(16, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)))
+
+    @classmethod
+    @contextlib.contextmanager
+    def _host_threads(cls):
+        old = torch.get_num_threads()
+        if old < cls.THREADS:
+            torch.set_num_threads(cls.THREADS)
+        try:
+            yield
+        finally:
+            if old < cls.THREADS:
+                torch.set_num_threads(old)
 
     @classmethod
     def _get(cls):
@@ -212,7 +227,7 @@ class Staging:
     @classmethod
     def download(cls, pairs) -> None:
         """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)], same lengths."""
-        with cls._lock:
+        with cls._lock, cls._host_threads():
             cls._download(pairs)
 
     @classmethod
@@ -239,7 +254,7 @@ class Staging:
     def upload(cls, pairs) -> None:
         """pairs: [(contiguous CUDA uint8 view, contiguous CPU uint8 view)]; returns once
         every chunk is enqueued (the host array may be reused: it has been read)."""
-        with cls._lock:
+        with cls._lock, cls._host_threads():
             cls._upload(pairs)
 
     @classmethod
