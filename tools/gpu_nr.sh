@@ -1,5 +1,6 @@
-# narrow-ring passes (tall_nr_kernel) and the 16-column diagonal SpMM: parity
-# tests, isolated timings at n = 2^24 against variants, the step
+# narrow-ring passes (tall_nr_kernel): parity tests, isolated timings at n = 2^24 against
+# variant libraries, the step.  Build the variants first (they are not kept in the tree):
+#   python tools/ab_build.py nonr="-DRG_TALL_NR=0" nr3="-DRG_NR_CTAS=3"
 set -x
 timeout 900 python -m pytest tests/test_gpu_kernels.py -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_nr.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_nr.log
