@@ -553,3 +553,30 @@ def test_spmm_diagonal_layout_bitwise(cuda, case, p):
     assert np.array_equal(y_csr, ref, equal_nan=True)
     assert np.array_equal(y_dia, ref, equal_nan=True)
     assert np.array_equal(y_rng, ref, equal_nan=True)
+
+
+# ---------------------------------------------------------------- staged host <-> device copies
+
+
+@pytest.mark.parametrize("dtype", ["f64", "c128"])
+def test_staged_block_copies_round_trip_bitwise(cuda, dtype):
+    """device.Staging (large copies through two page-locked chunks): blocks
+    whose columns cross chunk boundaries, with a padded leading dimension
+    (n not a multiple of 32), and a 1-D index array, come back bit for bit."""
+    D = _dev()
+    rng = np.random.default_rng(12)
+    n = (D.Staging.CHUNK // 8) + 12345  # one f64 column = a full chunk + a tail
+    p = 2
+    A = rng.standard_normal((n, p))
+    if dtype == "c128":
+        A = A + 1j * rng.standard_normal((n, p))
+    A = np.asfortranarray(A)
+    assert A.nbytes >= D.Staging.MIN_BYTES and D.round_ld(n) != n
+    dt = torch.complex128 if dtype == "c128" else torch.float64
+    Ad = D.to_device_block(A, cuda, dt)
+    assert D.ld_of(Ad) == D.round_ld(n)
+    assert torch.equal(Ad.cpu(), torch.from_numpy(A))           # upload
+    back = D.to_numpy_block(Ad)                                   # download
+    assert back.flags.f_contiguous and np.array_equal(back, A)
+    idx = rng.integers(0, 2**31 - 1, size=D.Staging.CHUNK // 4 * 2 + 7, dtype=np.int32)
+    assert np.array_equal(D.upload_array(idx, cuda).cpu().numpy(), idx)
